@@ -1,0 +1,226 @@
+/*
+ * packinfer.h — C ABI of the B200-native PackInfer hot path (arXiv 2602.06072).
+ *
+ * The interface follows the paper's statement of the problem (Alg. 1 KwIn/KwOut, PAPER.md
+ * P:205-206): inputs are the batch R (per-request lengths, prefix lineage), the group
+ * capacity C and the paged KV cache M_paged; outputs are the groups {S_g}, the contiguous
+ * buffers {B_g} and the offset tables {O_g}, plus the packed attention over the "union of
+ * valid query-key regions" and the lossless merge of split requests.
+ * It is exported as a FlashAttention-style drop-in: varlen Q/O, fp32 LSE.
+ *
+ * Conventions (every entry point):
+ *   - returns pi_status; never throws; never allocates device memory; never synchronises a
+ *     stream (device work is enqueued on the caller's stream, like cuBLAS).
+ *   - the caller owns every buffer; pointers marked "device" must be device memory of the
+ *     current CUDA device, "host" pointers host memory.
+ *   - invalid arguments return PI_EINVAL with no side effects (details: packinfer_last_error);
+ *     asynchronous device faults surface at the caller's next synchronisation.
+ *   - an empty batch (n = 0) is valid: planning returns zero counts, device calls are no-ops.
+ *   - thread-safe across distinct plans/streams; the library keeps no global mutable state
+ *     beyond a thread-local error string and cached CUDA function attributes.
+ *   - plans are reproducible: identical inputs give byte-identical host tables.
+ *
+ * Element layouts (all row-major, innermost last):
+ *   q, out        [total_q, q_row_stride] elements; the local Q heads of token t start at
+ *                 q + t*q_row_stride, head h at + h*head_dim (varlen, caller order: request i
+ *                 owns rows q_off[i] .. q_off[i]+q_len[i]-1, q_off = exclusive cumsum of q_len)
+ *   lse           fp32 [hq_count, total_q]   (natural log; hq_count = hkv_count * gqa_ratio)
+ *   k/v_paged     [num_blocks, page_size, hkv_total, head_dim]          (D6)
+ *   block_table   int32 [n + n_prefix, max_blocks]: row i < n maps request i's logical tokens
+ *                 [0, kv_len[i]) (a shared prefix's physical blocks first); row n + p maps
+ *                 prefix p's tokens [0, prefix_len[p]).
+ *   k/v_buf       [hkv_count, buffer_tokens, head_dim]  group-contiguous buffers B_g laid end
+ *                 to end (base_g = sum of earlier group capacities)       (Alg. 1 Part 2)
+ *   partial_o     fp32 [n_partial_slots, hq_count, head_dim]; partial_lse fp32
+ *                 [n_partial_slots, hq_count] — partial results of split rows (reading R10).
+ */
+#ifndef PACKINFER_H_
+#define PACKINFER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PI_API __attribute__((visibility("default")))
+#else
+#define PI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* pi_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  PI_OK = 0,
+  PI_EINVAL = -1, /* invalid argument (see packinfer_last_error)                         */
+  PI_ENOSPC = -2, /* caller buffer too small; required sizes were written back          */
+  PI_ECUDA = -3,  /* a CUDA runtime/driver call failed (launch or tensor-map encode)     */
+  PI_EUNSUP = -4  /* unsupported dtype / head_dim / device (needs sm_100a)              */
+} pi_status;
+
+typedef enum { PI_BF16 = 0, PI_FP32 = 1 } pi_dtype; /* FP32 runs tcgen05 kind::tf32       */
+
+/* Static string for a status code. */
+PI_API const char* packinfer_strerror(pi_status s);
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+PI_API const char* packinfer_last_error(void);
+/* Library version string. */
+PI_API const char* packinfer_version(void);
+
+/* ------------------------------------------------------------------------------------------
+ * Planner configuration (Alg. 1 inputs; defaults from Table tab:hyperparams).
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t capacity;     /* C, max prefix-deduplicated tokens per group (Eq. 2); default
+                           8192.  Requests with kv_len > C are split into pieces of C
+                           tokens (reading R5).  Must be >= 1.                         */
+  int32_t num_groups;   /* initial G override; 0 => max(1, ceil(L_dedup / C)) (Alg.1 l.1,
+                           P:212; reading R2)                                                */
+  int64_t mem_cap;      /* M_max in tokens incl. headroom (Eq. 2 second term); 0 disables it;
+                           else must be >= capacity + headroom                              */
+  int32_t headroom;     /* delta: tokens reserved after every suffix; >= 0        */
+  int32_t tile_q;       /* rows per packed work tile; must be 128 (tcgen05 M=128)            */
+  int32_t tile_k;       /* keys per K tile; must be 128 (P:159 T in {128,256})               */
+  int32_t decode_chunk; /* max keys per decode work item (multiple of tile_k; e.g. 1024)      */
+  int32_t gqa_ratio;    /* r = Hq / Hkv in [1, 16]: decode rows are (request, GQA head)       */
+} pi_config;
+
+/* Fill *cfg with the defaults: C=8192, G auto, no M_max, delta=0, 128/128 tiles,
+ * decode_chunk=1024, gqa_ratio=1. */
+PI_API void packinfer_default_config(pi_config* cfg);
+
+/* ---- plan tables (host, written by packinfer_plan; compared bit-exactly with the oracle) -- */
+typedef struct { int32_t request, piece, kv_begin, kv_len, group; } pi_piece;
+/* O_g entry (Alg. 1 l.12): (Delta_prefix, L_P, Delta_suffix, L_Q), group-local.     */
+typedef struct { int32_t d_prefix, l_prefix, d_suffix, l_suffix; } pi_offset;
+/* Group S_g: global buffer base, L(S_g) (dedup tokens), member count, capacity incl. delta. */
+typedef struct { int64_t base; int32_t load, members, cap, reserved; } pi_group;
+/* Copy(M_paged[src] -> B_g): src_kind 0 = request block table row src_id, 1 = prefix src_id;
+ * logical tokens [src_begin, src_begin+len) -> buffer tokens [dst, dst+len).                */
+typedef struct { int32_t src_kind, src_id, src_begin, len; int64_t dst; } pi_copy;
+
+/* ---- packed execution domain (implementation-side; checked by the coverage invariant) ---- */
+/* A work item: <= tile_q query rows attending over span_count key spans (buffer tokens).
+ * Every span but the last is fully visible to every row; in the last span row r sees keys
+ * [rows[r].lo, rows[r].hi).  Items are LPT-sorted by n_ktiles (descending).               */
+typedef struct {
+  int32_t kind;       /* 0 = prefill (rows are tokens, one Q head per launch unit)
+                         1 = decode  (rows are (request, GQA head), one KV head per unit)   */
+  int32_t group;      /* group of the last span                                             */
+  int32_t row_begin, row_count;
+  int32_t span_begin, span_count;
+  int32_t n_ktiles;   /* cost: sum over spans of ceil(len / tile_k)                         */
+  int32_t reserved;
+} pi_work;
+/* A query row: token index into q/out, visible interval [lo, hi) in the last span, and
+ * out = ((slot + 1) << 4) | h_sub, slot = -1 for a direct write, h_sub = GQA sub-head
+ * (decode rows; 0 for prefill rows).                                                       */
+typedef struct { int32_t q_token, lo, hi, out; } pi_row;
+typedef struct { int32_t begin, len; } pi_span;
+/* Merge entry: output token q_token combines partial slots [slot_begin, slot_begin+count). */
+typedef struct { int32_t q_token, slot_begin, slot_count, reserved; } pi_merge;
+
+typedef struct {
+  /* all pointers point into the caller's host arena (packinfer_plan) */
+  pi_piece* pieces;    int32_t n_pieces;
+  pi_offset* offsets;  /* indexed like pieces */
+  pi_group* groups;    int32_t n_groups;   int32_t g0;
+  pi_copy* copies;     int32_t n_copies;
+  int64_t* copy_prefix;                    /* [n_copies+1] cumsum of cells per copy: len (+ headroom
+                                              after a suffix); copy_prefix[n_copies] == buffer_tokens */
+  pi_work* prefill_work; int32_t n_prefill_work;
+  pi_work* decode_work;  int32_t n_decode_work;
+  pi_row* rows;        int32_t n_rows;
+  pi_span* spans;      int32_t n_spans;
+  pi_merge* merges;    int32_t n_merges;   int32_t n_partial_slots;
+  int64_t buffer_tokens;                   /* sum of group capacities                    */
+  int64_t copy_tokens;                     /* Eq. 5 volume = sum of loads                */
+  int32_t n_requests, n_prefix, total_q, gqa_ratio;
+  int64_t eta_num, eta_den;                /* literal Eq. 1 with T = tile_k       */
+  int64_t valid_cells, tile_cells;         /* prefill tile efficiency (reading R-eta)     */
+  int32_t discrepancy;                     /* Eq. 3                               */
+  int32_t reserved;
+  void* arena;  size_t arena_bytes;        /* the host arena holding every table          */
+} pi_plan;
+
+/* Alg. 1 Parts 1-2 plus the packed execution domain.
+ *   n, kv_len[n] (>= 1), q_len[n] (1 <= q_len <= kv_len; the last q_len positions are the
+ *   queries; q_len == 1 rows take the decode path), prefix_id[n] (-1 = none, else
+ *   < n_prefix; may be NULL), prefix_len[n_prefix] (1 <= prefix_len[p] <= kv_len - q_len of
+ *   every member).  All host pointers.
+ *   host_arena/arena_bytes: caller host memory (pinned memory makes the upload async).
+ *   If arena_bytes is too small returns PI_ENOSPC and sets out->arena_bytes to the size
+ *   needed (two-call sizing; NULL/0 is allowed for the first call).                        */
+PI_API pi_status packinfer_plan(int32_t n, const int32_t* kv_len, const int32_t* q_len,
+                         const int32_t* prefix_id, int32_t n_prefix, const int32_t* prefix_len,
+                         const pi_config* cfg, void* host_arena, size_t arena_bytes,
+                         pi_plan* out);
+
+/* Device view of a plan: the same tables in device memory. */
+typedef struct {
+  const pi_copy* copies;  const int64_t* copy_prefix; int32_t n_copies; int64_t copy_tokens;
+  const pi_work* prefill_work; int32_t n_prefill_work;
+  const pi_work* decode_work;  int32_t n_decode_work;
+  const pi_row* rows;  const pi_span* spans;
+  const pi_merge* merges; int32_t n_merges; int32_t n_partial_slots;
+  int64_t buffer_tokens;
+  int32_t n_requests, total_q, gqa_ratio, tile_k;
+} pi_device_plan;
+
+/* Enqueue one host->device copy of plan->arena into dev_arena (device, >= plan->arena_bytes,
+ * 256-byte aligned) on `stream` and fill *out with device pointers into dev_arena.        */
+PI_API pi_status packinfer_plan_upload(const pi_plan* plan, void* dev_arena, size_t dev_bytes,
+                                pi_stream_t stream, pi_device_plan* out);
+
+/* ------------------------------------------------------------------------------------------
+ * Contiguous memory consolidation (Alg. 1 Copy lines P:244/P:250; §3.2):
+ * gather every copy-plan entry from the paged cache into k_buf/v_buf for KV heads
+ * [hkv_begin, hkv_begin + hkv_count).  Bitwise copy; headroom cells are not written.
+ * ---------------------------------------------------------------------------------------- */
+PI_API pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void* k_paged,
+                                const void* v_paged, const int32_t* block_table,
+                                int32_t max_blocks, int32_t page_size, int32_t hkv_total,
+                                int32_t hkv_begin, int32_t hkv_count, int32_t head_dim,
+                                pi_dtype dt, void* k_buf, void* v_buf, pi_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Packed attention ("union of valid query-key regions"; P:172 one launch for every
+ * group): ONE persistent launch over all prefill (resp. decode) work items x local heads.
+ * S = scale * Q K^T and O += P V run on tcgen05 (TMEM accumulators, TMA-fed K/V), softmax is
+ * online with fp32 statistics; bf16 inputs, fp32 accumulation, P rounded to bf16 (reading
+ * R13; PI_FP32 uses kind::tf32).  q/out: local heads [0, hkv_count*gqa_ratio) of each token
+ * (strides in elements); rows with a single result write out/lse directly, split rows write
+ * (o, lse) to partial slots for packinfer_merge.  head_dim in {64, 128}.
+ * lse may be NULL.  softmax_scale <= 0 selects 1/sqrt(head_dim).
+ * ---------------------------------------------------------------------------------------- */
+PI_API pi_status packinfer_attention_prefill(const pi_device_plan* dp, const void* q,
+                                      int64_t q_row_stride, const void* k_buf,
+                                      const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,
+                                      int32_t head_dim, float softmax_scale, pi_dtype dt,
+                                      void* out, int64_t out_row_stride, float* lse,
+                                      float* partial_o, float* partial_lse, pi_stream_t stream);
+
+PI_API pi_status packinfer_attention_decode(const pi_device_plan* dp, const void* q,
+                                     int64_t q_row_stride, const void* k_buf,
+                                     const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,
+                                     int32_t head_dim, float softmax_scale, pi_dtype dt,
+                                     void* out, int64_t out_row_stride, float* lse,
+                                     float* partial_o, float* partial_lse, pi_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Lossless LSE merge of split rows (reading R10):
+ *   M = max_b lse_b; w_b = exp(lse_b - M); o = sum w_b o_b / sum w_b; lse = M + ln sum w_b,
+ * empty partials (lse = -inf) carry zero weight.  Writes out (dt) and lse for every merge
+ * entry and every local head.
+ * ---------------------------------------------------------------------------------------- */
+PI_API pi_status packinfer_merge(const pi_device_plan* dp, const float* partial_o,
+                          const float* partial_lse, int32_t hq_count, int32_t head_dim,
+                          pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
+                          pi_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACKINFER_H_ */

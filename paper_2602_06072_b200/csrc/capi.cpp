@@ -1,0 +1,104 @@
+// C ABI entry points that need no device code: status strings, config defaults, planning and
+// plan upload.  Device entry points live next to their kernels (relayout.cu, attention.cu,
+// merge.cu).
+#include <cstring>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "packinfer.h"
+
+namespace pi {
+namespace {
+thread_local std::string g_last_error;
+}
+pi_status fail(pi_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+pi_status ok() {
+  g_last_error.clear();
+  return PI_OK;
+}
+}  // namespace pi
+
+extern "C" {
+
+const char* packinfer_strerror(pi_status s) {
+  switch (s) {
+    case PI_OK: return "ok";
+    case PI_EINVAL: return "invalid argument";
+    case PI_ENOSPC: return "buffer too small";
+    case PI_ECUDA: return "CUDA error";
+    case PI_EUNSUP: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* packinfer_last_error(void) { return pi::g_last_error.c_str(); }
+
+const char* packinfer_version(void) { return "packinfer-b200 0.1 (sm_100a)"; }
+
+void packinfer_default_config(pi_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->capacity = 8192;
+  cfg->num_groups = 0;
+  cfg->mem_cap = 0;
+  cfg->headroom = 0;
+  cfg->tile_q = 128;
+  cfg->tile_k = 128;
+  cfg->decode_chunk = 1024;
+  cfg->gqa_ratio = 1;
+}
+
+pi_status packinfer_plan(int32_t n, const int32_t* kv_len, const int32_t* q_len,
+                         const int32_t* prefix_id, int32_t n_prefix, const int32_t* prefix_len,
+                         const pi_config* cfg, void* host_arena, size_t arena_bytes,
+                         pi_plan* out) {
+  pi_status s = pi::plan_impl(n, kv_len, q_len, prefix_id, n_prefix, prefix_len, cfg,
+                              host_arena, arena_bytes, out);
+  if (s == PI_OK) pi::ok();
+  return s;
+}
+
+pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, size_t dev_bytes,
+                                pi_stream_t stream, pi_device_plan* out) {
+  if (!p || !out) return pi::fail(PI_EINVAL, "plan and out must be non-NULL");
+  if (!p->arena) return pi::fail(PI_EINVAL, "plan has no host arena (planning failed?)");
+  if (!dev_arena || dev_bytes < p->arena_bytes)
+    return pi::fail(PI_ENOSPC, "device arena too small: need " + std::to_string(p->arena_bytes));
+  if (reinterpret_cast<uintptr_t>(dev_arena) % 256)
+    return pi::fail(PI_EINVAL, "device arena must be 256-byte aligned");
+  cudaError_t e = cudaMemcpyAsync(dev_arena, p->arena, p->arena_bytes, cudaMemcpyHostToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return pi::fail(PI_ECUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  const char* H = static_cast<const char*>(p->arena);
+  char* D = static_cast<char*>(dev_arena);
+  auto dev = [&](const void* h) -> const void* {
+    return h ? static_cast<const void*>(D + (static_cast<const char*>(h) - H)) : nullptr;
+  };
+  std::memset(out, 0, sizeof(*out));
+  out->copies = static_cast<const pi_copy*>(dev(p->copies));
+  out->copy_prefix = static_cast<const int64_t*>(dev(p->copy_prefix));
+  out->n_copies = p->n_copies;
+  out->copy_tokens = p->copy_tokens;
+  out->prefill_work = static_cast<const pi_work*>(dev(p->prefill_work));
+  out->n_prefill_work = p->n_prefill_work;
+  out->decode_work = static_cast<const pi_work*>(dev(p->decode_work));
+  out->n_decode_work = p->n_decode_work;
+  out->rows = static_cast<const pi_row*>(dev(p->rows));
+  out->spans = static_cast<const pi_span*>(dev(p->spans));
+  out->merges = static_cast<const pi_merge*>(dev(p->merges));
+  out->n_merges = p->n_merges;
+  out->n_partial_slots = p->n_partial_slots;
+  out->buffer_tokens = p->buffer_tokens;
+  out->n_requests = p->n_requests;
+  out->total_q = p->total_q;
+  out->gqa_ratio = p->gqa_ratio;
+  out->tile_k = 128;
+  return pi::ok();
+}
+
+}  // extern "C"

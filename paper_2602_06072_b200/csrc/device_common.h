@@ -1,0 +1,31 @@
+// Host helpers shared by the CUDA translation units: TMA tensor-map encoding through the driver
+// entry point (no -lcuda link dependency) and cached device properties.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "common.h"
+#include "packinfer.h"
+
+namespace pi {
+
+// Encodes a rank-3 tiled tensor map (innermost first).  Returns PI_OK or PI_ECUDA/PI_EUNSUP.
+pi_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
+                         const uint64_t dims[3], const uint64_t strides_bytes[2],
+                         const uint32_t box[3], CUtensorMapSwizzle swizzle);
+
+// Number of SMs of the current device (cached per device).
+int num_sms();
+
+// Fails with PI_EUNSUP unless the current device is compute capability 10.0 (sm_100a).
+pi_status require_sm100();
+
+inline pi_status cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PI_OK;
+  return fail(PI_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace pi

@@ -1,0 +1,134 @@
+// Contiguous memory consolidation (PackInfer §3.2; Alg. 1 Copy lines P:244/P:250).
+//
+// Gathers every copy-plan entry from the paged KV cache [num_blocks, page, Hkv, d] into the
+// group-contiguous buffers [hkv_count, buffer_tokens, d].  One warp per buffer token: it reads
+// the token's hkv_count*d contiguous elements (all local heads of one paged slot: coalesced) and
+// scatters them into the per-head buffers.  Cells in a suffix's headroom (delta) are
+// written with zeros so every buffer cell is finite (the attention kernels read whole 128-key
+// tiles; masked keys meet P = 0, which must not multiply NaN garbage).
+// HBM-bound: algorithmic bytes = 2 (K,V) x copied tokens x hkv_count x d x elem (read + write).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_common.h"
+#include "packinfer.h"
+
+namespace pi {
+
+struct RelayoutParams {
+  const pi_copy* copies;
+  const int64_t* ext_prefix;  // [n_copies + 1] cumsum of buffer cells per copy (len + headroom)
+  int32_t n_copies;
+  int64_t total;              // == buffer_tokens
+  int32_t n_requests;
+  const uint8_t* kp;
+  const uint8_t* vp;
+  const int32_t* bt;
+  int32_t max_blocks;
+  int32_t page;
+  int64_t token_bytes;        // hkv_total * d * es  (one paged slot, all heads)
+  int64_t head_off_bytes;     // hkv_begin * d * es
+  int32_t chunks;             // hkv_count * d * es / 16
+  int32_t head_chunks;        // d * es / 16
+  int64_t buf_head_bytes;     // buffer_tokens * d * es
+  uint8_t* kb;
+  uint8_t* vb;
+};
+
+__global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
+  const int64_t g = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= p.total) return;
+  // copy entry containing buffer cell g: largest c with ext_prefix[c] <= g
+  int lo = 0, hi = p.n_copies - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&p.ext_prefix[mid]) <= g) lo = mid; else hi = mid - 1;
+  }
+  const pi_copy cp = p.copies[lo];
+  const int64_t off = g - p.ext_prefix[lo];
+  const int64_t dst = cp.dst + off;
+  const int64_t row_bytes = (int64_t)p.head_chunks * 16;
+  constexpr int U = 8;  // up to 8 x 16 B per lane in flight per tensor
+  if (off < cp.len) {
+    const int row = cp.src_kind == 0 ? cp.src_id : p.n_requests + cp.src_id;
+    const int64_t j = cp.src_begin + off;
+    const int blk = __ldg(&p.bt[(int64_t)row * p.max_blocks + j / p.page]);
+    const int64_t src = ((int64_t)blk * p.page + j % p.page) * p.token_bytes + p.head_off_bytes;
+    for (int base = 0; base < p.chunks; base += 32 * U) {
+      uint4 kv[U], vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * 32 + lane;
+        if (i < p.chunks) {
+          kv[u] = __ldg(reinterpret_cast<const uint4*>(p.kp + src) + i);
+          vv[u] = __ldg(reinterpret_cast<const uint4*>(p.vp + src) + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * 32 + lane;
+        if (i < p.chunks) {
+          const int h = i / p.head_chunks, c = i % p.head_chunks;
+          const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)c * 16;
+          *reinterpret_cast<uint4*>(p.kb + d) = kv[u];
+          *reinterpret_cast<uint4*>(p.vb + d) = vv[u];
+        }
+      }
+    }
+  } else {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < p.chunks; i += 32) {
+      const int h = i / p.head_chunks, c = i % p.head_chunks;
+      const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)c * 16;
+      *reinterpret_cast<uint4*>(p.kb + d) = z;
+      *reinterpret_cast<uint4*>(p.vb + d) = z;
+    }
+  }
+}
+
+}  // namespace pi
+
+extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void* k_paged, const void* v_paged,
+                                           const int32_t* block_table, int32_t max_blocks, int32_t page_size,
+                                           int32_t hkv_total, int32_t hkv_begin, int32_t hkv_count,
+                                           int32_t head_dim, pi_dtype dt, void* k_buf, void* v_buf,
+                                           pi_stream_t stream) {
+  using namespace pi;
+  if (!dp) return fail(PI_EINVAL, "device plan is NULL");
+  if (dp->buffer_tokens == 0) return ok();
+  if (!k_paged || !v_paged || !block_table || !k_buf || !v_buf) return fail(PI_EINVAL, "NULL pointer argument");
+  if (max_blocks < 1 || page_size < 1) return fail(PI_EINVAL, "max_blocks and page_size must be >= 1");
+  if (hkv_total < 1 || hkv_begin < 0 || hkv_count < 1 || hkv_begin + hkv_count > hkv_total)
+    return fail(PI_EINVAL, "KV head range out of bounds");
+  if (dt != PI_BF16 && dt != PI_FP32) return fail(PI_EUNSUP, "dtype must be PI_BF16 or PI_FP32");
+  const int es = dt == PI_BF16 ? 2 : 4;
+  if ((head_dim * es) % 16) return fail(PI_EINVAL, "head_dim * element size must be a multiple of 16 bytes");
+  if ((reinterpret_cast<uintptr_t>(k_paged) | reinterpret_cast<uintptr_t>(v_paged) |
+       reinterpret_cast<uintptr_t>(k_buf) | reinterpret_cast<uintptr_t>(v_buf)) % 16)
+    return fail(PI_EINVAL, "tensors must be 16-byte aligned");
+  RelayoutParams p{};
+  p.copies = dp->copies;
+  p.ext_prefix = dp->copy_prefix;
+  p.n_copies = dp->n_copies;
+  p.total = dp->buffer_tokens;
+  p.n_requests = dp->n_requests;
+  p.kp = static_cast<const uint8_t*>(k_paged);
+  p.vp = static_cast<const uint8_t*>(v_paged);
+  p.bt = block_table;
+  p.max_blocks = max_blocks;
+  p.page = page_size;
+  p.token_bytes = (int64_t)hkv_total * head_dim * es;
+  p.head_off_bytes = (int64_t)hkv_begin * head_dim * es;
+  p.head_chunks = head_dim * es / 16;
+  p.chunks = hkv_count * p.head_chunks;
+  p.buf_head_bytes = dp->buffer_tokens * head_dim * es;
+  p.kb = static_cast<uint8_t*>(k_buf);
+  p.vb = static_cast<uint8_t*>(v_buf);
+  const int64_t blocks = (p.total + 7) / 8;
+  if (blocks > 0x7fffffff) return fail(PI_EINVAL, "buffer too large");
+  relayout_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  pi_status s = cuda_check(cudaGetLastError(), "relayout_kernel launch");
+  return s == PI_OK ? ok() : s;
+}

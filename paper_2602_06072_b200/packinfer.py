@@ -1,0 +1,327 @@
+"""Thin Python binding of libpackinfer.so (include/packinfer.h) — argument marshalling only.
+
+Every step of the hot path runs inside the library: the planner in C++, relayout / attention /
+merge in sm_100a CUDA kernels.  torch is used for device memory, streams and pinned host
+memory.  There is NO CPU fallback: if the shared library is missing or was built for another
+architecture, every call raises.
+
+Function names mirror the C ABI (packinfer_plan, packinfer_relayout_kv,
+packinfer_attention_prefill, packinfer_attention_decode, packinfer_merge); PackedBatch strings
+them together for one batch step.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpackinfer.so")
+
+PI_OK, PI_EINVAL, PI_ENOSPC, PI_ECUDA, PI_EUNSUP = 0, -1, -2, -3, -4
+PI_BF16, PI_FP32 = 0, 1
+
+EXPORTS = [
+    "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
+    "packinfer_plan", "packinfer_plan_upload", "packinfer_relayout_kv",
+    "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_merge",
+]
+
+
+class PackInferError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status}: {detail}")
+        self.status = status
+
+
+# ----------------------------------------------------------------------------- C structs
+class pi_config(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("num_groups", C.c_int32), ("mem_cap", C.c_int64),
+                ("headroom", C.c_int32), ("tile_q", C.c_int32), ("tile_k", C.c_int32),
+                ("decode_chunk", C.c_int32), ("gqa_ratio", C.c_int32)]
+
+
+PIECE_DT = np.dtype([("request", "<i4"), ("piece", "<i4"), ("kv_begin", "<i4"), ("kv_len", "<i4"), ("group", "<i4")])
+OFFSET_DT = np.dtype([("d_prefix", "<i4"), ("l_prefix", "<i4"), ("d_suffix", "<i4"), ("l_suffix", "<i4")])
+GROUP_DT = np.dtype([("base", "<i8"), ("load", "<i4"), ("members", "<i4"), ("cap", "<i4"), ("reserved", "<i4")])
+COPY_DT = np.dtype([("src_kind", "<i4"), ("src_id", "<i4"), ("src_begin", "<i4"), ("len", "<i4"), ("dst", "<i8")])
+WORK_DT = np.dtype([("kind", "<i4"), ("group", "<i4"), ("row_begin", "<i4"), ("row_count", "<i4"),
+                    ("span_begin", "<i4"), ("span_count", "<i4"), ("n_ktiles", "<i4"), ("reserved", "<i4")])
+ROW_DT = np.dtype([("q_token", "<i4"), ("lo", "<i4"), ("hi", "<i4"), ("out", "<i4")])
+SPAN_DT = np.dtype([("begin", "<i4"), ("len", "<i4")])
+MERGE_DT = np.dtype([("q_token", "<i4"), ("slot_begin", "<i4"), ("slot_count", "<i4"), ("reserved", "<i4")])
+
+
+class pi_plan(C.Structure):
+    _fields_ = [("pieces", C.c_void_p), ("n_pieces", C.c_int32),
+                ("offsets", C.c_void_p),
+                ("groups", C.c_void_p), ("n_groups", C.c_int32), ("g0", C.c_int32),
+                ("copies", C.c_void_p), ("n_copies", C.c_int32),
+                ("copy_prefix", C.c_void_p),
+                ("prefill_work", C.c_void_p), ("n_prefill_work", C.c_int32),
+                ("decode_work", C.c_void_p), ("n_decode_work", C.c_int32),
+                ("rows", C.c_void_p), ("n_rows", C.c_int32),
+                ("spans", C.c_void_p), ("n_spans", C.c_int32),
+                ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
+                ("buffer_tokens", C.c_int64), ("copy_tokens", C.c_int64),
+                ("n_requests", C.c_int32), ("n_prefix", C.c_int32), ("total_q", C.c_int32),
+                ("gqa_ratio", C.c_int32),
+                ("eta_num", C.c_int64), ("eta_den", C.c_int64),
+                ("valid_cells", C.c_int64), ("tile_cells", C.c_int64),
+                ("discrepancy", C.c_int32), ("reserved", C.c_int32),
+                ("arena", C.c_void_p), ("arena_bytes", C.c_size_t)]
+
+
+class pi_device_plan(C.Structure):
+    _fields_ = [("copies", C.c_void_p), ("copy_prefix", C.c_void_p), ("n_copies", C.c_int32),
+                ("copy_tokens", C.c_int64),
+                ("prefill_work", C.c_void_p), ("n_prefill_work", C.c_int32),
+                ("decode_work", C.c_void_p), ("n_decode_work", C.c_int32),
+                ("rows", C.c_void_p), ("spans", C.c_void_p),
+                ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
+                ("buffer_tokens", C.c_int64),
+                ("n_requests", C.c_int32), ("total_q", C.c_int32), ("gqa_ratio", C.c_int32),
+                ("tile_k", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libpackinfer.so (raises if it is missing — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise PackInferError(PI_EUNSUP, "load", f"{_LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(_LIB_PATH)
+        vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+        L.packinfer_strerror.restype = C.c_char_p
+        L.packinfer_strerror.argtypes = [C.c_int]
+        L.packinfer_last_error.restype = C.c_char_p
+        L.packinfer_version.restype = C.c_char_p
+        L.packinfer_default_config.argtypes = [C.POINTER(pi_config)]
+        L.packinfer_plan.restype = C.c_int
+        L.packinfer_plan.argtypes = [i32, vp, vp, vp, i32, vp, C.POINTER(pi_config), vp, C.c_size_t,
+                                     C.POINTER(pi_plan)]
+        L.packinfer_plan_upload.restype = C.c_int
+        L.packinfer_plan_upload.argtypes = [C.POINTER(pi_plan), vp, C.c_size_t, vp, C.POINTER(pi_device_plan)]
+        L.packinfer_relayout_kv.restype = C.c_int
+        L.packinfer_relayout_kv.argtypes = [C.POINTER(pi_device_plan), vp, vp, vp, i32, i32, i32, i32, i32, i32,
+                                            C.c_int, vp, vp, vp]
+        for name in ("packinfer_attention_prefill", "packinfer_attention_decode"):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = [C.POINTER(pi_device_plan), vp, i64, vp, vp, i32, i32, i32, f32, C.c_int, vp, i64, vp,
+                          vp, vp, vp]
+        L.packinfer_merge.restype = C.c_int
+        L.packinfer_merge.argtypes = [C.POINTER(pi_device_plan), vp, vp, i32, i32, C.c_int, vp, i64, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != PI_OK:
+        raise PackInferError(st, where, lib().packinfer_last_error().decode())
+
+
+def version() -> str:
+    return lib().packinfer_version().decode()
+
+
+def default_config(**kw) -> pi_config:
+    cfg = pi_config()
+    lib().packinfer_default_config(C.byref(cfg))
+    for k, v in kw.items():
+        setattr(cfg, k, int(v))
+    return cfg
+
+
+# ----------------------------------------------------------------------------- planning
+@dataclass
+class HostPlan:
+    """Result of packinfer_plan: the C struct plus numpy views of its tables (host arena)."""
+    c: pi_plan
+    arena: object            # keeps the host arena alive (torch pinned tensor or numpy array)
+
+    def _view(self, name, n, dt):
+        ptr = getattr(self.c, name)
+        if n == 0 or not ptr:
+            return np.zeros(0, dt)
+        buf = (C.c_char * (n * dt.itemsize)).from_address(ptr)
+        return np.frombuffer(buf, dtype=dt, count=n)
+
+    @property
+    def pieces(self): return self._view("pieces", self.c.n_pieces, PIECE_DT)
+    @property
+    def offsets(self): return self._view("offsets", self.c.n_pieces, OFFSET_DT)
+    @property
+    def groups(self): return self._view("groups", self.c.n_groups, GROUP_DT)
+    @property
+    def copies(self): return self._view("copies", self.c.n_copies, COPY_DT)
+    @property
+    def copy_prefix(self): return self._view("copy_prefix", self.c.n_copies + 1, np.dtype("<i8"))
+    @property
+    def prefill_work(self): return self._view("prefill_work", self.c.n_prefill_work, WORK_DT)
+    @property
+    def decode_work(self): return self._view("decode_work", self.c.n_decode_work, WORK_DT)
+    @property
+    def rows(self): return self._view("rows", self.c.n_rows, ROW_DT)
+    @property
+    def spans(self): return self._view("spans", self.c.n_spans, SPAN_DT)
+    @property
+    def merges(self): return self._view("merges", self.c.n_merges, MERGE_DT)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def packinfer_plan(kv_len, q_len, prefix_id=None, prefix_len=(), cfg: Optional[pi_config] = None,
+                   pinned: bool = False, arena=None) -> HostPlan:
+    """Alg. 1 Parts 1-2 + packed execution domain (two-call sizing handled here)."""
+    L = lib()
+    kv, q = _i32(kv_len), _i32(q_len)
+    n = int(kv.shape[0])
+    pid = None if prefix_id is None else _i32(prefix_id)
+    pl = _i32(prefix_len) if len(prefix_len) else np.zeros(1, np.int32)
+    n_prefix = len(prefix_len)
+    cfg = cfg or default_config()
+    out = pi_plan()
+    ptr = lambda a: None if a is None else a.ctypes.data
+    for _ in range(2):
+        if arena is None:
+            st = L.packinfer_plan(n, ptr(kv), ptr(q), ptr(pid), n_prefix, ptr(pl), C.byref(cfg), None, 0, C.byref(out))
+        else:
+            st = L.packinfer_plan(n, ptr(kv), ptr(q), ptr(pid), n_prefix, ptr(pl), C.byref(cfg),
+                                  _arena_ptr(arena), _arena_bytes(arena), C.byref(out))
+        if st == PI_ENOSPC:
+            arena = _alloc_arena(int(out.arena_bytes), pinned)
+            continue
+        _check(st, "packinfer_plan")
+        return HostPlan(out, arena)
+    raise PackInferError(PI_ENOSPC, "packinfer_plan", "arena sizing did not converge")
+
+
+def _alloc_arena(nbytes: int, pinned: bool):
+    if pinned:
+        import torch
+        return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    return np.empty(nbytes, dtype=np.uint8)
+
+
+def _arena_ptr(a) -> int:
+    return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+
+def _arena_bytes(a) -> int:
+    return a.numel() if hasattr(a, "numel") else a.nbytes
+
+
+# ----------------------------------------------------------------------------- device calls
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def packinfer_plan_upload(plan: HostPlan, dev_arena, stream=None) -> pi_device_plan:
+    dp = pi_device_plan()
+    _check(lib().packinfer_plan_upload(C.byref(plan.c), dev_arena.data_ptr(), dev_arena.numel(),
+                                       _stream_ptr(stream), C.byref(dp)), "packinfer_plan_upload")
+    return dp
+
+
+def _dt(t) -> int:
+    import torch
+    if t.dtype == torch.bfloat16:
+        return PI_BF16
+    if t.dtype == torch.float32:
+        return PI_FP32
+    raise PackInferError(PI_EUNSUP, "dtype", f"unsupported dtype {t.dtype}")
+
+
+def packinfer_relayout_kv(dp: pi_device_plan, k_paged, v_paged, block_table, k_buf, v_buf,
+                          hkv_begin: int = 0, hkv_count: Optional[int] = None, stream=None):
+    nb, page, hkv_total, d = k_paged.shape
+    hkv_count = hkv_total - hkv_begin if hkv_count is None else hkv_count
+    _check(lib().packinfer_relayout_kv(C.byref(dp), k_paged.data_ptr(), v_paged.data_ptr(), block_table.data_ptr(),
+                                       block_table.shape[1], page, hkv_total, hkv_begin, hkv_count, d, _dt(k_paged),
+                                       k_buf.data_ptr(), v_buf.data_ptr(), _stream_ptr(stream)),
+           "packinfer_relayout_kv")
+
+
+def _attention(fn, name, dp, q, k_buf, v_buf, out, lse, partial_o, partial_lse, gqa_ratio, scale, stream):
+    hkv_count, _, d = k_buf.shape
+    _check(getattr(lib(), fn)(C.byref(dp), q.data_ptr(), q.stride(0), k_buf.data_ptr(), v_buf.data_ptr(),
+                              hkv_count, gqa_ratio, d, float(scale), _dt(q), out.data_ptr(), out.stride(0),
+                              None if lse is None else lse.data_ptr(),
+                              None if partial_o is None else partial_o.data_ptr(),
+                              None if partial_lse is None else partial_lse.data_ptr(), _stream_ptr(stream)), name)
+
+
+def packinfer_attention_prefill(dp, q, k_buf, v_buf, out, lse=None, partial_o=None, partial_lse=None,
+                                gqa_ratio: int = 1, scale: float = 0.0, stream=None):
+    _attention("packinfer_attention_prefill", "packinfer_attention_prefill", dp, q, k_buf, v_buf, out, lse,
+               partial_o, partial_lse, gqa_ratio, scale, stream)
+
+
+def packinfer_attention_decode(dp, q, k_buf, v_buf, out, lse=None, partial_o=None, partial_lse=None,
+                               gqa_ratio: int = 1, scale: float = 0.0, stream=None):
+    _attention("packinfer_attention_decode", "packinfer_attention_decode", dp, q, k_buf, v_buf, out, lse,
+               partial_o, partial_lse, gqa_ratio, scale, stream)
+
+
+def packinfer_merge(dp, partial_o, partial_lse, out, lse=None, stream=None):
+    n_slots, hq, d = partial_o.shape
+    _check(lib().packinfer_merge(C.byref(dp), partial_o.data_ptr(), partial_lse.data_ptr(), hq, d, _dt(out),
+                                 out.data_ptr(), out.stride(0), None if lse is None else lse.data_ptr(),
+                                 _stream_ptr(stream)), "packinfer_merge")
+
+
+# ----------------------------------------------------------------------------- one batch step
+class PackedBatch:
+    """Plans a batch once and runs the hot path: upload -> relayout -> prefill -> decode -> merge.
+
+    q: [total_q, Hq_local, d] (varlen, request order); k/v_paged: [blocks, page, Hkv, d]; the
+    local KV heads are [hkv_begin, hkv_begin + hkv_count) (KV-head sharding)."""
+
+    def __init__(self, kv_len, q_len, prefix_id, prefix_len, hkv_count: int, gqa_ratio: int, head_dim: int,
+                 dtype, device, capacity: int = 8192, headroom: int = 0, num_groups: int = 0,
+                 decode_chunk: int = 1024, mem_cap: int = 0):
+        import torch
+        self.cfg = default_config(capacity=capacity, headroom=headroom, num_groups=num_groups,
+                                  decode_chunk=decode_chunk, gqa_ratio=gqa_ratio, mem_cap=mem_cap)
+        self.args = (kv_len, q_len, prefix_id, prefix_len)
+        self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, pinned=True)
+        self.device = torch.device(device)
+        self.hkv, self.r, self.d, self.dtype = hkv_count, gqa_ratio, head_dim, dtype
+        c = self.plan.c
+        self.dev_arena = torch.empty(max(int(c.arena_bytes), 256), dtype=torch.uint8, device=self.device)
+        self.dp = packinfer_plan_upload(self.plan, self.dev_arena)
+        bt = max(int(c.buffer_tokens), 1)
+        self.k_buf = torch.empty((hkv_count, bt, head_dim), dtype=dtype, device=self.device)
+        self.v_buf = torch.empty_like(self.k_buf)
+        hq = hkv_count * gqa_ratio
+        ns = max(int(c.n_partial_slots), 1)
+        self.partial_o = torch.empty((ns, hq, head_dim), dtype=torch.float32, device=self.device)
+        self.partial_lse = torch.empty((ns, hq), dtype=torch.float32, device=self.device)
+
+    def replan(self, stream=None):
+        """Host planning + plan upload (the per-step host part of the hot path)."""
+        kv_len, q_len, prefix_id, prefix_len = self.args
+        self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, arena=self.plan.arena)
+        self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
+
+    def run(self, q, k_paged, v_paged, block_table, out, lse=None, hkv_begin: int = 0, stream=None,
+            relayout: bool = True):
+        if relayout:
+            packinfer_relayout_kv(self.dp, k_paged, v_paged, block_table, self.k_buf, self.v_buf,
+                                  hkv_begin, self.hkv, stream)
+        packinfer_attention_prefill(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
+                                    self.partial_lse, self.r, 0.0, stream)
+        packinfer_attention_decode(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
+                                   self.partial_lse, self.r, 0.0, stream)
+        packinfer_merge(self.dp, self.partial_o, self.partial_lse, out, lse, stream)
