@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""PackInfer hot-path benchmark (BASELINE.json metric: packed prefill TFLOP/s & decode KV HBM GB/s
+vs B200 peak; batch step latency).
+
+One STEP = one pass of the whole hot path over one batch:
+    packinfer_plan (host C++) -> plan upload (H2D) -> packinfer_relayout_kv -> packed prefill
+    -> packed decode -> LSE merge
+Headline workload (N=1): BASELINE.json configs[1], the Llama-3-8B-shaped heterogeneous prefill
+batch (64 requests, 16..8192 tokens; 32 Q / 8 KV heads, d=128, bf16).  value = algorithmic
+prefill FLOPs / step time (TFLOP/s).  The decode row (configs[2], 256 requests, KV 32..32k) is
+reported under "decode" (GB/s of Eq. 5 KV bytes).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--shard group|heads]
+Multi-GPU (torchrun, one process per GPU): default --shard group = weak scaling, rank r runs
+its own batch (seed 0 + r; groups of independent sub-batches, no collective on the data path);
+--shard heads = strong scaling by KV head over one batch.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------- workloads
+def make_workload(name: str, seed: int):
+    from synth import workloads as W
+    if name == "cfg2":
+        return W.cfg2_prefill(seed)
+    if name == "cfg3":
+        return W.cfg3_decode(seed + 1)
+    if name == "cfg4_decode":
+        return W.cfg4_decode(seed + 2)
+    raise ValueError(name)
+
+
+def algorithmic(b, plan_c, hkv_local):
+    """Algorithmic work of one step: prefill FLOPs over visible pairs only; decode
+    bytes = Eq. 5 KV volume of the decode requests + their Q and O."""
+    r = b.hq // b.hkv
+    flops = 0
+    for L, q in zip(b.kv_len.tolist(), b.q_len.tolist()):
+        if q > 1:
+            flops += q * (L - q) + q * (q + 1) // 2
+    flops *= 4 * b.d * hkv_local * r
+    es = 2 if b.dtype == "bf16" else 4
+    dec_tokens = int(plan_c.copy_tokens) if (b.q_len == 1).all() else None
+    kv_bytes = None if dec_tokens is None else 2 * dec_tokens * hkv_local * b.d * es
+    qo_bytes = 2 * int((b.q_len == 1).sum()) * hkv_local * r * b.d * es
+    return flops, kv_bytes, qo_bytes
+
+
+class Runner:
+    """Owns the device state of one batch and runs steps on one stream (double-buffered plans)."""
+
+    def __init__(self, b, device, hkv_begin, hkv_count, capacity=8192, headroom=0, seed=0):
+        import torch
+        from synth import workloads as W
+        from paper_2602_06072_b200 import packinfer as pk
+        self.pk, self.torch, self.b = pk, torch, b
+        self.r = b.hq // b.hkv
+        self.hkv_begin, self.hkv_count = hkv_begin, hkv_count
+        self.t = W.make_tensors(b, device=device, seed=seed)
+        dt = self.t["q"].dtype
+        self.pbs = [pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, hkv_count, self.r, b.d, dt,
+                                   device, capacity=capacity, headroom=headroom) for _ in range(2)]
+        self.events = [torch.cuda.Event() for _ in range(2)]
+        for e in self.events:
+            e.record()
+        self.q = self.t["q"][:, hkv_begin * self.r:(hkv_begin + hkv_count) * self.r]
+        self.out = torch.empty((b.total_q, hkv_count * self.r, b.d), dtype=dt, device=device)
+        self.lse = torch.empty((hkv_count * self.r, b.total_q), dtype=torch.float32, device=device)
+        self.stream = torch.cuda.current_stream()
+        c = self.pbs[0].plan.c
+        self.launches_per_step = 1 + (c.n_prefill_work > 0) + (c.n_decode_work > 0) + (c.n_merges > 0)
+        self.kernel_events = []
+
+    def step(self, i, time_kernel=False):
+        pk, torch = self.pk, self.torch
+        pb = self.pbs[i % 2]
+        self.events[i % 2].synchronize()            # host arena of this slot no longer read by H2D
+        pb.replan(self.stream)                       # host planner + async upload
+        self.events[i % 2].record(self.stream)
+        pk.packinfer_relayout_kv(pb.dp, self.t["k_paged"], self.t["v_paged"], self.t["block_table"], pb.k_buf,
+                                 pb.v_buf, self.hkv_begin, self.hkv_count, self.stream)
+        if time_kernel:
+            e0, e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), \
+                torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+        pk.packinfer_attention_prefill(pb.dp, self.q, pb.k_buf, pb.v_buf, self.out, self.lse, pb.partial_o,
+                                       pb.partial_lse, self.r, 0.0, self.stream)
+        if time_kernel:
+            e1.record(self.stream)
+        pk.packinfer_attention_decode(pb.dp, self.q, pb.k_buf, pb.v_buf, self.out, self.lse, pb.partial_o,
+                                      pb.partial_lse, self.r, 0.0, self.stream)
+        if time_kernel:
+            e2.record(self.stream)
+            self.kernel_events.append((e0, e1, e2))
+        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, self.out, self.lse, self.stream)
+
+    def kernel_ms(self):
+        pre = [a.elapsed_time(b) for a, b, _ in self.kernel_events]
+        dec = [b.elapsed_time(c) for _, b, c in self.kernel_events]
+        return (sum(pre) / len(pre) if pre else 0.0), (sum(dec) / len(dec) if dec else 0.0)
+
+
+def timed_steps(runner, steps, warmup, dist_on):
+    import torch
+    for i in range(warmup):
+        runner.step(i)
+    torch.cuda.synchronize()
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    runner.kernel_events.clear()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(steps):
+        runner.step(warmup + i, time_kernel=True)
+    e.record()
+    torch.cuda.synchronize()
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+    return s.elapsed_time(e)
+
+
+def e2e_steps(b, runner, steps):
+    """Same metric through the public API with HOST buffers: every step copies the step's inputs
+    H2D from pinned memory, runs the hot path, and reads the output back D2H."""
+    import torch
+    t = runner.t
+    host = {k: v.cpu().pin_memory() for k, v in t.items()}
+    out_h = torch.empty(runner.out.shape, dtype=runner.out.dtype).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = out_h.numel() * out_h.element_size()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(steps):
+        for k in t:
+            t[k].copy_(host[k], non_blocking=True)
+        runner.step(10_000 + i)
+        out_h.copy_(runner.out, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps, h2d, d2h
+
+
+# ------------------------------------------------------------------------------- oracle timing
+def oracle_sample(b, budget_s: float, seed: int):
+    """Times the oracle (as it stands) on a bounded sample of the workload's requests on this
+    host.  Returns (algorithmic FLOP/s or KV bytes/s, seconds, description, cores)."""
+    import torch
+    from oracle import attention as OA
+    from synth import workloads as W
+    cores = len(os.sched_getaffinity(0))
+    t = W.make_tensors(b, device="cpu", seed=seed)
+    order = np.argsort(b.kv_len)                      # short requests first, then longer ones
+    done, flops, kv_bytes, t0 = [], 0, 0, time.time()
+    for i in order:
+        if time.time() - t0 > budget_s:
+            break
+        OA.attention(t["q"], t["k_paged"], t["v_paged"], t["block_table"], b.kv_len, b.q_len, b.page_size,
+                     requests=[int(i)])
+        L, q = int(b.kv_len[i]), int(b.q_len[i])
+        flops += 4 * b.d * b.hq * (q * (L - q) + q * (q + 1) // 2)
+        kv_bytes += 2 * L * b.hkv * b.d * 2
+        done.append(int(i))
+    dt = time.time() - t0
+    desc = (f"{len(done)}/{b.n} requests of {b.name} (shortest first, {int(b.kv_len[done].sum())} KV tokens), "
+            f"fp64 numpy, {dt:.1f}s")
+    return flops, kv_bytes, dt, desc, cores
+
+
+def run_reference(args, cfg_name):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    b = make_workload(cfg_name, 0)
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(b, per_step, 0)
+    vals, secs = [], []
+    desc, cores = "", 1
+    for _ in range(args.steps):
+        f, kvb, dt, desc, cores = oracle_sample(b, per_step, 0)
+        vals.append(f / dt / 1e12)
+        secs.append(dt)
+    v = sum(vals) / len(vals)
+    line = {"impl": "reference", "metric": "packed prefill TFLOP/s (cfg2 step)", "value": v, "unit": "TFLOP/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * sum(secs) / len(secs), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": b.name, "requests": b.n, "hq": b.hq, "hkv": b.hkv, "head_dim": b.d},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="packinfer", choices=["packinfer", "reference"])
+    ap.add_argument("--shard", default="group", choices=["group", "heads"])
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args, "cfg2")
+        return
+
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peak_src = load_peaks()
+    dev = torch.device("cuda", local)
+
+    b = make_workload("cfg2", 0 if args.shard == "heads" else rank)
+    if args.shard == "heads" and world > 1:
+        assert b.hkv % world == 0
+        hc = b.hkv // world
+        h0 = rank * hc
+    else:
+        h0, hc = 0, b.hkv
+    runner = Runner(b, dev, h0, hc, seed=b.seed)
+    flops, _, _ = algorithmic(b, runner.pbs[0].plan.c, hc)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    total_ms = timed_steps(runner, args.steps, args.warmup, dist_on)
+    clocks = sampler.stop()
+    ms_step = total_ms / args.steps
+    pre_ms, _ = runner.kernel_ms()
+    if dist_on:
+        import torch.distributed as dist
+        tt = torch.tensor([ms_step, pre_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step, pre_ms = float(tt[0]), float(tt[1])
+    units_total = flops * (world if args.shard == "group" else 1)
+    value = units_total / (ms_step * 1e-3) / 1e12
+    pc = runner.pbs[0].plan.c
+    achieved = flops / (pre_ms * 1e-3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("prefill_attention_dram_bytes")
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "kernel": "packed_attention_kernel<128,bf16> (prefill)", "kernel_ms": pre_ms,
+                "peak_source": peak_src + " bf16 burst", "frac_of_sustained": achieved / peaks.get(
+                    "bf16_tflops_sustained", peaks["bf16_tflops"]),
+                "tile_efficiency": pc.valid_cells / max(1, pc.tile_cells)}
+
+    result = {"metric": "packed prefill TFLOP/s (cfg2 batch step)", "value": value, "unit": "TFLOP/s",
+              "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+              "higher_is_better": True, "scaling": "weak" if args.shard == "group" else "strong",
+              "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+              "config": {"workload": b.name + " (BASELINE.json configs[1])", "requests": b.n,
+                         "tokens": int(b.kv_len.sum()), "hq": b.hq, "hkv": b.hkv, "head_dim": b.d,
+                         "capacity": 8192, "groups": int(pc.n_groups), "work_items": int(pc.n_prefill_work),
+                         "step": "plan+upload+relayout+prefill(+decode+merge)",
+                         "l2": "inputs larger than L2 (paged KV 224 MB + Q 448 MB per step > 126 MB)",
+                         "parallelism": f"{args.shard}-sharded x{world}", "algorithmic_tflop": flops / 1e12},
+              "roofline": roofline, "clocks": clocks,
+              "gpu_launches": runner.launches_per_step * args.steps}
+
+    if not args.no_decode:
+        bd = make_workload("cfg3", 0 if args.shard == "heads" else rank)
+        rd = Runner(bd, dev, h0, hc, seed=bd.seed)
+        _, kvb, qob = algorithmic(bd, rd.pbs[0].plan.c, hc)
+        dms = timed_steps(rd, max(3, args.steps), args.warmup, dist_on) / max(3, args.steps)
+        _, dec_ms = rd.kernel_ms()
+        ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
+        result["decode"] = {"workload": bd.name + " (BASELINE.json configs[2])", "ms_per_step": dms,
+                            "kernel_ms": dec_ms, "kv_bytes": kvb, "achieved_gbs": ach, "peak_gbs": peaks["hbm_gbs"],
+                            "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
+                            "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9,
+                            "work_items": int(rd.pbs[0].plan.c.n_decode_work),
+                            "partial_slots": int(rd.pbs[0].plan.c.n_partial_slots)}
+        result["decode"]["gpu_launches"] = rd.launches_per_step * max(3, args.steps)
+        del rd
+
+    if not args.no_e2e:
+        e_ms, h2d, d2h = e2e_steps(b, runner, max(2, min(args.steps, 5)))
+        result["e2e"] = {"value": units_total / (e_ms * 1e-3) / 1e12,
+                         "unit": "TFLOP/s", "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        f, kvb, dt, desc, cores = oracle_sample(b, args.cpu_budget, b.seed)
+        result["cpu_baseline"] = {"value": f / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                                  "sample": desc}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist_on:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

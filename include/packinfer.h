@@ -60,7 +60,12 @@ typedef enum {
   PI_EUNSUP = -4  /* unsupported dtype / head_dim / device (needs sm_100a)              */
 } pi_status;
 
-typedef enum { PI_BF16 = 0, PI_FP32 = 1 } pi_dtype; /* FP32 runs tcgen05 kind::tf32       */
+typedef enum {
+  PI_BF16 = 0,         /* bf16 operands, bf16 out/in-place results (tcgen05 kind::f16)          */
+  PI_FP32 = 1,         /* fp32 operands and output (tcgen05 kind::tf32; head_dim 64)            */
+  PI_BF16_OUT_F32 = 2  /* bf16 operands, fp32 output: isolates kernel arithmetic from output
+                          rounding (reading R13); for attention/merge only                      */
+} pi_dtype;
 
 /* Static string for a status code. */
 PI_API const char* packinfer_strerror(pi_status s);

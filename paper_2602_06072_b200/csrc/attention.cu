@@ -48,6 +48,7 @@ struct AttnParams {
   float* partial_o;
   float* partial_lse;
   float scale_log2;        // softmax_scale * log2(e)
+  int32_t out_f32;         // 1: write out as fp32 (bf16 operands, fp32 output mode)
   const uint8_t* v_buf;    // fp32 path only: V staged transposed by warp 3
   int64_t buffer_tokens;
 };
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(256, 1)
       const bool warp_any = wq * 32 < wk.row_count;
       pi_row row = {0, 0, 0, 0};
       if (valid) row = p.rows[wk.row_begin + row_id];
-      float m_ref = NEG_INF, l = 0.f;
+      float m_ref = NEG_INF, l = 0.f, lr = 0.f;
       uint32_t j = 0;
       for (int s = 0; s < wk.span_count; ++s) {
         const pi_span sp = p.spans[wk.span_begin + s];
@@ -364,6 +365,7 @@ __global__ void __launch_bounds__(256, 1)
             tmem_wait_st();
             if (need) {
               l *= alpha;
+              lr *= alpha;
               m_ref = m_new;
             }
           }
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&bar[B_PDONE], (tt & 1) ^ 1);  // previous P.V finished reading P
           if (valid) {
             const bool live = (m_ref != NEG_INF);
-            float psum = 0.f;
+            float psum = 0.f, prsum = 0.f;
             uint8_t* prow = smem + p_gen_base + row_id * 128;
             if constexpr (!F32) {
 #pragma unroll
@@ -383,8 +385,11 @@ __global__ void __launch_bounds__(256, 1)
                 for (int e = 0; e < 4; ++e) {
                   const float a = live ? ex2(__uint_as_float(sr[cc * 8 + 2 * e]) - m_ref) : 0.f;
                   const float b = live ? ex2(__uint_as_float(sr[cc * 8 + 2 * e + 1]) - m_ref) : 0.f;
-                  psum += a + b;
                   pk[e] = pack_bf16(a, b);
+                  psum += a + b;
+                  // O is normalised with the P the tensor core actually multiplies (bf16-rounded);
+                  // the LSE keeps the exact fp32 sum
+                  prsum += __uint_as_float(pk[e] << 16) + __uint_as_float(pk[e] & 0xffff0000u);
                 }
                 uint4* dst = reinterpret_cast<uint4*>(prow + (cc >> 3) * C::ATOM_BYTES +
                                                       (((cc & 7) ^ (row_id & 7)) << 4));
@@ -398,6 +403,7 @@ __global__ void __launch_bounds__(256, 1)
                 for (int e = 0; e < 4; ++e) {
                   pv[e] = live ? ex2(__uint_as_float(sr[cc * 4 + e]) - m_ref) : 0.f;
                   psum += pv[e];
+                  prsum += pv[e];
                 }
                 uint4* dst = reinterpret_cast<uint4*>(prow + (cc >> 3) * C::ATOM_BYTES +
                                                       (((cc & 7) ^ (row_id & 7)) << 4));
@@ -406,6 +412,7 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
             l += psum;
+            lr += prsum;
           }
           fence_proxy_async_smem();
           tc_fence_before();
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t tlast = t + j - 1;
       mbar_wait(&bar[B_PDONE], tlast & 1);
       tc_fence_after();
-      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+      const float inv_l = lr > 0.f ? 1.0f / lr : 0.f;
       const float lse_v = l > 0.f ? (m_ref + __log2f(l)) * 0.69314718055994530942f : NEG_INF;
       const int slot = (row.out >> 4) - 1;
       const int hsub = row.out & 15;
@@ -430,8 +437,9 @@ __global__ void __launch_bounds__(256, 1)
           reg_fence(o32);
           if (valid) {
             if (slot < 0) {
-              uint8_t* dst = p.out + ((int64_t)row.q_token * p.out_row_stride + (int64_t)head * D + c4 * 32) * C::ES;
-              if constexpr (!F32) {
+              const int oes = (F32 || p.out_f32) ? 4 : 2;
+              uint8_t* dst = p.out + ((int64_t)row.q_token * p.out_row_stride + (int64_t)head * D + c4 * 32) * oes;
+              if (!F32 && !p.out_f32) {
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                   uint32_t pk[4];
@@ -481,7 +489,7 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 template <int D, bool F32>
-static pi_status launch(const pi_device_plan* dp, bool decode, const void* q, int64_t q_row_stride,
+static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, const void* q, int64_t q_row_stride,
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                         cudaStream_t stream) {
@@ -507,6 +515,7 @@ static pi_status launch(const pi_device_plan* dp, bool decode, const void* q, in
   p.partial_lse = partial_lse;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.v_buf = static_cast<const uint8_t*>(v_buf);
+  p.out_f32 = out_f32 ? 1 : 0;
   p.buffer_tokens = dp->buffer_tokens;
 
   CUtensorMap tmK, tmV;
@@ -546,7 +555,10 @@ static pi_status attention_entry(bool decode, const pi_device_plan* dp, const vo
   if (decode && gqa_ratio != dp->gqa_ratio)
     return fail(PI_EINVAL, "gqa_ratio differs from the plan's (decode rows are planned per GQA head)");
   if (head_dim != 64 && head_dim != 128) return fail(PI_EUNSUP, "head_dim must be 64 or 128");
-  if (dt != PI_BF16 && dt != PI_FP32) return fail(PI_EUNSUP, "dtype must be PI_BF16 or PI_FP32");
+  if (dt != PI_BF16 && dt != PI_FP32 && dt != PI_BF16_OUT_F32)
+    return fail(PI_EUNSUP, "dtype must be PI_BF16, PI_FP32 or PI_BF16_OUT_F32");
+  const bool out_f32 = dt == PI_BF16_OUT_F32;
+  if (out_f32) dt = PI_BF16;
   if (dt == PI_FP32 && head_dim != 64) return fail(PI_EUNSUP, "PI_FP32 supports head_dim 64 only");
   if (q_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim || out_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim)
     return fail(PI_EINVAL, "row stride smaller than the local heads");
@@ -560,13 +572,13 @@ static pi_status attention_entry(bool decode, const pi_device_plan* dp, const vo
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)head_dim);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dt == PI_BF16 && head_dim == 128)
-    s = launch<128, false>(dp, decode, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+    s = launch<128, false>(dp, decode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                            out_row_stride, lse, partial_o, partial_lse, st);
   else if (dt == PI_BF16 && head_dim == 64)
-    s = launch<64, false>(dp, decode, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+    s = launch<64, false>(dp, decode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                           out_row_stride, lse, partial_o, partial_lse, st);
   else
-    s = launch<64, true>(dp, decode, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+    s = launch<64, true>(dp, decode, false, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                          out_row_stride, lse, partial_o, partial_lse, st);
   return s == PI_OK ? ok() : s;
 }

@@ -68,6 +68,7 @@ extern "C" pi_status packinfer_merge(const pi_device_plan* dp, const float* part
   const int64_t warps = (int64_t)dp->n_merges * hq_count;
   const unsigned blocks = (unsigned)((warps + 7) / 8);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dt == PI_BF16_OUT_F32) dt = PI_FP32;  // output element type is what the merge writes
   uint8_t* o = static_cast<uint8_t*>(out);
   if (dt == PI_BF16 && head_dim == 128)
     merge_kernel<128, false><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,

@@ -22,7 +22,7 @@ import numpy as np
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpackinfer.so")
 
 PI_OK, PI_EINVAL, PI_ENOSPC, PI_ECUDA, PI_EUNSUP = 0, -1, -2, -3, -4
-PI_BF16, PI_FP32 = 0, 1
+PI_BF16, PI_FP32, PI_BF16_OUT_F32 = 0, 1, 2
 
 EXPORTS = [
     "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
@@ -254,9 +254,13 @@ def packinfer_relayout_kv(dp: pi_device_plan, k_paged, v_paged, block_table, k_b
 
 
 def _attention(fn, name, dp, q, k_buf, v_buf, out, lse, partial_o, partial_lse, gqa_ratio, scale, stream):
+    import torch
     hkv_count, _, d = k_buf.shape
+    dt = _dt(q)
+    if dt == PI_BF16 and out.dtype == torch.float32:
+        dt = PI_BF16_OUT_F32
     _check(getattr(lib(), fn)(C.byref(dp), q.data_ptr(), q.stride(0), k_buf.data_ptr(), v_buf.data_ptr(),
-                              hkv_count, gqa_ratio, d, float(scale), _dt(q), out.data_ptr(), out.stride(0),
+                              hkv_count, gqa_ratio, d, float(scale), dt, out.data_ptr(), out.stride(0),
                               None if lse is None else lse.data_ptr(),
                               None if partial_o is None else partial_o.data_ptr(),
                               None if partial_lse is None else partial_lse.data_ptr(), _stream_ptr(stream)), name)

@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Gate (BASELINE.json north star): bf16 inputs / fp32 accumulation within 1e-2 max-abs and 1e-3
+mean-abs of the oracle; relayout bitwise; LSE within 1e-3 (fp32 statistics; tf32 toy: 5e-3).
+Sizes span several 128-row/128-key tiles, ragged tails, packed short requests, shared
+prefixes, split requests (C small) and decode chunks with partials + merge."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as OA
+from oracle import layout as OL
+from oracle import plan as OP
+from synth import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("tests.gpu_helpers")
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("C,delta", [(8192, 0), (300, 5), (128, 0)])
+def test_relayout_bitwise(C, delta):
+    b = W.random_batch(1, n=12, max_len=500, hq=8, hkv=4, d=128, n_prefix=2)
+    t = W.make_tensors(b, device="cuda")
+    _, _, pb = H.run_batch(b, t, C=C, delta=delta)
+    op = OP.plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, C, headroom=delta)
+    for buf_gpu, src in ((pb.k_buf, "k_paged"), (pb.v_buf, "v_paged")):
+        want, valid = OL.expected_buffers(op.copies, t[src].cpu(), t["block_table"].cpu(), b.n, b.page_size,
+                                          op.buffer_tokens)
+        got = buf_gpu.cpu().view(torch.int16).numpy()
+        assert np.array_equal(got[:, valid], want[:, valid])
+        assert (got[:, ~valid] == 0).all()           # headroom zero-filled
+
+
+def test_relayout_head_slice():
+    b = W.random_batch(2, n=6, max_len=300, hq=8, hkv=4, d=64)
+    t = W.make_tensors(b, device="cuda")
+    _, _, pb = H.run_batch(b, t, hkv_begin=1, hkv_count=2)
+    op = OP.plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, 8192)
+    want, valid = OL.expected_buffers(op.copies, t["k_paged"].cpu(), t["block_table"].cpu(), b.n, b.page_size,
+                                      op.buffer_tokens, heads=[1, 2])
+    got = pb.k_buf.cpu().view(torch.int16).numpy()
+    assert np.array_equal(got[:, valid], want[:, valid])
+
+
+@pytest.mark.parametrize("C,chunk", [(8192, 1024), (128, 128)])
+@pytest.mark.parametrize("maker", [W.toy_prefill, W.toy_decode])
+def test_toy_fp32(maker, C, chunk):
+    b = maker()
+    t = W.make_tensors(b, device="cuda")
+    out, lse, _ = H.run_batch(b, t, C=C, decode_chunk=chunk)
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out, lse, ro, rl, lse_tol=5e-3)
+
+
+@pytest.mark.parametrize("out_f32", [False, True])
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("d", [64, 128])
+def test_random_mixed_bf16(seed, d, out_f32):
+    rng = np.random.default_rng(seed)
+    hkv = int(rng.choice([1, 2, 4]))
+    r = int(rng.choice([1, 4, 8]))
+    b = W.random_batch(100 + seed, n=int(rng.integers(3, 14)), max_len=int(rng.integers(40, 900)), hq=hkv * r,
+                       hkv=hkv, d=d, n_prefix=2, page_size=128 if seed % 2 else 256)
+    C = int(rng.choice([8192, 512, 200]))
+    t = W.make_tensors(b, device="cuda")
+    out, lse, _ = H.run_batch(b, t, C=C, delta=int(rng.integers(0, 9)), decode_chunk=128 * int(rng.integers(1, 4)),
+                              out_f32=out_f32)
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out, lse, ro, rl)
+
+
+def test_peaky_queries():
+    """q x 4 stresses the max-subtraction / lazy rescale path."""
+    b = W.random_batch(77, n=8, max_len=800, hq=8, hkv=2, d=128)
+    t = W.make_tensors(b, device="cuda", peaky=4.0)
+    for out_f32 in (False, True):
+        out, lse, _ = H.run_batch(b, t, C=300, decode_chunk=256, out_f32=out_f32)
+        ro, rl = H.oracle_full(b, t)
+        H.compare(out, lse, ro, rl)
+
+
+def test_mask_probe():
+    """q = 0, V channel 0 = request id (exact in bf16): any cross-request leak moves o[0]; exp(lse)
+    must count exactly the causally visible keys (pos + 1)."""
+    b = W.random_batch(55, n=10, max_len=600, hq=4, hkv=2, d=128, n_prefix=0)
+    t = W.make_tensors(b, device="cuda")
+    t["q"].zero_()
+    bt = t["block_table"].cpu().numpy()
+    t["v_paged"][..., 0] = -1.0
+    for i in range(b.n):
+        for j in range(-(-int(b.kv_len[i]) // b.page_size)):
+            t["v_paged"][int(bt[i, j]), :, :, 0] = float(i)
+    out, lse, _ = H.run_batch(b, t, C=256, decode_chunk=128)
+    o = out.float().cpu().numpy()
+    l = lse.cpu().numpy()
+    off = 0
+    for i in range(b.n):
+        L, ql = int(b.kv_len[i]), int(b.q_len[i])
+        for tq in range(ql):
+            assert np.all(o[off + tq, :, 0] == float(i)), (i, tq)
+            assert np.all(np.round(np.exp(l[:, off + tq].astype(np.float64))) == L - ql + tq + 1), (i, tq)
+        off += ql
+
+
+def test_head_sharding_bitwise():
+    """KV-head sharding: a rank computing heads [h0, h1) gets bitwise the 1-GPU result."""
+    b = W.random_batch(9, n=8, max_len=500, hq=8, hkv=4, d=128)
+    t = W.make_tensors(b, device="cuda")
+    full, full_lse, _ = H.run_batch(b, t, C=300)
+    for h0, hc in ((0, 2), (2, 2), (1, 1), (3, 1)):
+        part, plse, _ = H.run_batch(b, t, C=300, hkv_begin=h0, hkv_count=hc)
+        r = b.hq // b.hkv
+        assert torch.equal(part.view(torch.int16), full[:, h0 * r:(h0 + hc) * r].contiguous().view(torch.int16))
+        assert torch.equal(plse, full_lse[h0 * r:(h0 + hc) * r])
+
+
+def test_regroup_invariance():
+    """Outputs do not depend on the grouping (C, G): permuting/regrouping is lossless."""
+    b = W.random_batch(31, n=10, max_len=700, hq=4, hkv=2, d=128)
+    t = W.make_tensors(b, device="cuda")
+    ro, rl = H.oracle_full(b, t)
+    for C, G in ((8192, 0), (700, 0), (8192, 5), (150, 0)):
+        out, lse, _ = H.run_batch(b, t, C=C, num_groups=G, decode_chunk=256)
+        H.compare(out, lse, ro, rl)
+
+
+def test_empty_and_degenerate():
+    b = W.Batch("single-token", np.array([1], np.int32), np.array([1], np.int32), np.array([-1], np.int32),
+                np.zeros(0, np.int32), 2, 1, 128, "bf16", 128, 4)
+    t = W.make_tensors(b, device="cuda")
+    out, lse, _ = H.run_batch(b, t)
+    v0 = t["v_paged"][int(t["block_table"][0, 0]), 0, 0].float()
+    assert torch.equal(out[0, 0].float(), v0) and torch.equal(out[0, 1].float(), v0)   # 1 key -> o = v0
+    from paper_2602_06072_b200 import packinfer as pk
+    pb = pk.PackedBatch([], [], None, [], 1, 1, 128, torch.bfloat16, "cuda")
+    q = torch.empty((0, 1, 128), dtype=torch.bfloat16, device="cuda")
+    pb.run(q, t["k_paged"], t["v_paged"], t["block_table"], q.clone())
+    torch.cuda.synchronize()
+
+
+def _sampled_rows(b, rng, per_req=3):
+    rows = []
+    for i in range(b.n):
+        ql = int(b.q_len[i])
+        ts = {0, ql - 1} | set(rng.integers(0, ql, size=per_req).tolist())
+        rows += [(i, int(x)) for x in sorted(ts)]
+    return rows
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4_decode", "cfg4_prefill"])
+def test_full_size_sampled(name):
+    """BASELINE.json full sizes in bench.py's launch configuration; oracle on sampled rows."""
+    b = W.make_batch(name)
+    t = W.make_tensors(b, device="cuda")
+    out, lse, pb = H.run_batch(b, t, C=8192, delta=32 if "cfg4" in name else 0, out_f32=True)
+    rng = np.random.default_rng(0)
+    rows = _sampled_rows(b, rng)
+    ro, rl = OA.attention_rows(t["q"].cpu(), t["k_paged"].cpu(), t["v_paged"].cpu(), t["block_table"].cpu(),
+                               b.kv_len, b.q_len, b.page_size, rows)
+    q_off = np.concatenate([[0], np.cumsum(b.q_len)])
+    idx = torch.tensor([q_off[i] + tq for i, tq in rows], device="cuda")
+    o = out[idx].float().cpu().numpy()
+    l = lse[:, idx].cpu().numpy().T
+    err = np.abs(o - ro)
+    assert err.max() <= H.ATOL_MAX and err.mean() <= H.ATOL_MEAN, (err.max(), err.mean())
+    assert np.abs(l - rl).max() <= 1e-3
+    # property at any size: every row written (finite) exactly
+    assert torch.isfinite(out.float()).all()
