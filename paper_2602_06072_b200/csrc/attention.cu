@@ -1,21 +1,28 @@
 // Packed attention over the union of valid query-key regions (PackInfer §3.1): ONE
-// persistent launch per call covers every work item of every group (reading R18).
+// persistent launch per call covers every work item of every group (reading R17).
 //
-// Work unit = (work item, head).  A work item holds <= 128 query rows (prefill: tokens of one or
-// more packed requests; decode: (request, GQA sub-head) rows) and a list of key spans in
-// the group-contiguous KV buffers (Alg. 1 Part 2).  Every span but the last is visible to every
-// row; in the last span row r sees keys [lo_r, hi_r) (causal own-suffix / decode chunk).
+// Work item = <= 128 query rows (prefill: tokens of one or more packed requests; decode:
+// (request, GQA sub-head) rows) and a list of key spans in the group-contiguous KV
+// buffers (Alg. 1 Part 2).  Every span but the last is visible to every row; in the last span row
+// r sees keys [lo_r, hi_r) (causal own-suffix / decode chunk).
 //
-// Per CTA (one per SM, 256 threads, warp-specialised):
-//   warp 0  : TMA producer — K and V tiles (128 keys x head_dim, SWIZZLE_128B) into a 2-stage ring
-//   warp 1  : TMEM allocator + single-thread tcgen05.mma issuer:
-//               S_t = Q K_t^T  -> TMEM S[t%2]      (M=128, N=128, K=head_dim)
-//               O  += P_t V_t  -> TMEM O           (M=128, N=head_dim, K=128; V MN-major)
-//   warp 2  : Q gather — rows addressed through the plan's row table (cp.async, manual 128B swizzle)
-//   warps 4-7: softmax / correction / epilogue; thread i owns row i (= TMEM lane i), so the row max
-//             and sum need no cross-thread reduction.  Online softmax in the exp2 domain with a lazy
-//             rescale (O is rescaled in TMEM only when the running max grows by > 2^8).
-// bf16 operands run tcgen05 kind::f16, fp32 operands kind::tf32; accumulation is fp32 (R13).
+// Launch unit = (work item, KV head, Q-tile pair).  Prefill units carry TWO Q tiles — two query
+// heads of the same GQA group — which share every K/V tile and every mask, so one TMA stream feeds
+// two tensor-core pipelines.  Decode units carry one tile (its rows already span the GQA group).
+//
+// Per CTA (one per SM, 384 threads, warp-specialised):
+//   warp 0    TMA producer: K/V tiles (128 keys x d, SWIZZLE_128B) into a 2-stage ring
+//   warp 1    TMEM allocator + single-thread tcgen05.mma issuer, FA4-style ping-pong:
+//               S_X = Q_X K^T -> TMEM S_X     (SS, M=128 N=128 K=d)
+//               O_X += P_X V  -> TMEM O_X     (TS: P_X read from TMEM where it overwrote S_X)
+//             issue order  S_A0 S_B0 | PV_A0 S_A1 | PV_B0 S_B1 | PV_A1 S_A2 | ...
+//   warp 2    Q gather for both tiles through the plan's row table (cp.async, 128 B swizzle)
+//   warp 3    fp32 operands only: stages V^T (K-major) for kind::tf32
+//   warps 4-7 softmax / correction / epilogue of tile A; warps 8-11 of tile B.  Thread i owns
+//             row i (= TMEM lane i), so row max / sum need no shuffles.  Two TMEM passes per tile
+//             (max, then exp2 + pack + store P) keep register pressure low; the O rescale is lazy
+//             (only when the running max grows by > 2^8) and happens in TMEM.
+// bf16 operands run kind::f16, fp32 operands kind::tf32; accumulation fp32 (reading R13).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -35,7 +42,7 @@ struct AttnParams {
   const pi_row* rows;
   const pi_span* spans;
   int32_t n_work;
-  int32_t units;      // launch units per item: local Q heads (prefill) or local KV heads (decode)
+  int32_t units;      // launch units per item: hkv * ceil(r/2) (prefill) or hkv (decode)
   int32_t is_decode;
   int32_t r;          // GQA ratio
   const uint8_t* q;
@@ -61,31 +68,28 @@ struct AttnCfg {
   static constexpr int ATOM_ELEMS = 128 / ES;
   static constexpr int ATOM_BYTES = 128 * 128;        // one atom column of 128 rows
   static constexpr int TILE_BYTES = 128 * ROW_BYTES;  // 128 rows
-  static constexpr int P_ROW_BYTES = 128 * ES;        // 128 keys of P
-  static constexpr int P_BYTES = 128 * P_ROW_BYTES;
   static constexpr int NS = 2;                        // K/V pipeline stages
   static constexpr int QK_STEPS = ROW_BYTES / 32;     // MMAs per S tile (32 bytes of K each)
-  static constexpr int PV_STEPS = P_ROW_BYTES / 32;   // MMAs per O update
+  static constexpr int PV_STEPS = 128 * ES / 32;      // MMAs per O update (32 bytes of keys each)
   static constexpr int KEYS_PER_PV_STEP = 32 / ES;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + TILE_BYTES;
+  static constexpr int OFF_Q = 0;                     // Q_A, Q_B
+  static constexpr int OFF_K = 2 * TILE_BYTES;
   static constexpr int OFF_V = OFF_K + NS * TILE_BYTES;
-  static constexpr int OFF_P = OFF_V + NS * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;   // + barriers + alignment slack
   static constexpr uint32_t FMT = F32 ? 2u : 1u;
   static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 128, 0, 0);
-  // bf16: V is the MN-major B operand straight from TMA.  fp32 (kind::tf32): MN-major tf32 needs the
-  // 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
+  // bf16: V is the MN-major B operand straight from TMA.  fp32 (kind::tf32): MN-major tf32 needs
+  // the 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
   static constexpr uint32_t IDESC_PV = idesc_make(FMT, 128, D, 0, F32 ? 0 : 1);
   static constexpr int VT_ATOM_BYTES = D * 128;       // fp32 V^T: D rows x 32 keys
-  static constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O = 256;
+  static constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 enum BarId {
   B_QFULL = 0, B_QFREE, B_KFULL0, B_KFULL1, B_KFREE0, B_KFREE1, B_VFULL0, B_VFULL1, B_VFREE0, B_VFREE1,
-  B_SFULL0, B_SFULL1, B_SFREE0, B_SFREE1, B_PFULL, B_PDONE, B_OFREE, B_COUNT
+  B_SFULL0, B_SFULL1, B_PFULL0, B_PFULL1, B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_COUNT
 };
 
 // Makes the compiler treat r[] as produced after the preceding tcgen05.wait::ld.
@@ -95,8 +99,33 @@ __device__ __forceinline__ void reg_fence(uint32_t (&r)[N]) {
   for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
 }
 
+struct Unit {
+  pi_work wk;
+  int kvh;
+  int head0;   // Q head of tile A (tile B = head0 + 1); decode rows add their h_sub
+  bool has_b;
+};
+
+__device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
+  Unit u;
+  u.wk = p.work[w / p.units];
+  const int k = w % p.units;
+  if (p.is_decode) {
+    u.kvh = k;
+    u.head0 = k * p.r;
+    u.has_b = false;
+  } else {
+    const int pairs = (p.r + 1) >> 1;
+    u.kvh = k / pairs;
+    const int hp = k % pairs;
+    u.head0 = u.kvh * p.r + 2 * hp;
+    u.has_b = 2 * hp + 1 < p.r;
+  }
+  return u;
+}
+
 template <int D, bool F32>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     packed_attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV) {
   using C = AttnCfg<D, F32>;
@@ -118,11 +147,10 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&bar[B_VFULL0 + s], F32 ? 32 : 1);
       mbar_init(&bar[B_VFREE0 + s], 1);
       mbar_init(&bar[B_SFULL0 + s], 1);
-      mbar_init(&bar[B_SFREE0 + s], 128);
+      mbar_init(&bar[B_PFULL0 + s], 128);
+      mbar_init(&bar[B_OFULL0 + s], 1);
+      mbar_init(&bar[B_OFREE0 + s], 128);
     }
-    mbar_init(&bar[B_PFULL], 128);
-    mbar_init(&bar[B_PDONE], 1);
-    mbar_init(&bar[B_OFREE], 128);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -141,11 +169,9 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       uint32_t t = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const pi_work wk = p.work[w / p.units];
-        const int u = w % p.units;
-        const int kvh = p.is_decode ? u : u / p.r;
-        for (int s = 0; s < wk.span_count; ++s) {
-          const pi_span sp = p.spans[wk.span_begin + s];
+        const Unit u = get_unit(p, w);
+        for (int s = 0; s < u.wk.span_count; ++s) {
+          const pi_span sp = p.spans[u.wk.span_begin + s];
           for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
             const int st = t % C::NS;
             const uint32_t ph = (t / C::NS) & 1;
@@ -154,14 +180,14 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int a = 0; a < C::ATOMS; ++a)
               tma_load_3d(smem + C::OFF_K + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmK, &bar[B_KFULL0 + st],
-                          a * C::ATOM_ELEMS, k0, kvh);
+                          a * C::ATOM_ELEMS, k0, u.kvh);
             if constexpr (!F32) {
               mbar_wait(&bar[B_VFREE0 + st], ph ^ 1);
               mbar_arrive_expect_tx(&bar[B_VFULL0 + st], C::TILE_BYTES);
 #pragma unroll
               for (int a = 0; a < C::ATOMS; ++a)
                 tma_load_3d(smem + C::OFF_V + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmV, &bar[B_VFULL0 + st],
-                            a * C::ATOM_ELEMS, k0, kvh);
+                            a * C::ATOM_ELEMS, k0, u.kvh);
             }
           }
         }
@@ -172,51 +198,106 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       uint32_t t = 0, item = 0;
-      const uint32_t q_addr = sbase + C::OFF_Q;
-      const uint32_t p_addr = sbase + C::OFF_P;
-      auto issue_pv = [&](uint32_t tt, bool first) {
-        const int st = tt % C::NS;
-        mbar_wait(&bar[B_PFULL], tt & 1);
-        mbar_wait(&bar[B_VFULL0 + st], (tt / C::NS) & 1);
-        if (first) mbar_wait(&bar[B_OFREE], (item & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t v_addr = sbase + C::OFF_V + st * C::TILE_BYTES;
+      uint32_t cnt[2] = {0, 0};   // completions so far of SFULL/PFULL of region 0 / 1
+      uint32_t ix[2] = {0, 0};    // completions so far of OFULL/OFREE of slot 0 / 1
+      // S(X) = Q_X K(tt)^T into S/P region b
+      auto issue_s = [&](int X, int b, uint32_t tt) {
+        const uint32_t q_addr = sbase + C::OFF_Q + X * C::TILE_BYTES;
+        const uint32_t k_addr = sbase + C::OFF_K + (tt % C::NS) * C::TILE_BYTES;
+        const uint32_t d_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
+#pragma unroll
+        for (int kk = 0; kk < C::QK_STEPS; ++kk) {
+          const uint32_t off = (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32;
+          mma_ss<F32>(d_tmem, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
+                      C::IDESC_QK, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&bar[B_SFULL0 + b]);
+      };
+      // O_X += P(region b) V(tt)
+      auto issue_pv = [&](int X, int b, uint32_t tt, bool first) {
+        const uint32_t v_addr = sbase + C::OFF_V + (tt % C::NS) * C::TILE_BYTES;
+        const uint32_t p_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
+        const uint32_t d_tmem = tmem + (X ? C::TM_O1 : C::TM_O0);
 #pragma unroll
         for (int kk = 0; kk < C::PV_STEPS; ++kk) {
-          const uint64_t ad = sdesc_sw128(p_addr + (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = F32 ? sdesc_sw128(v_addr + (kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32, 16, 1024)
                                   : sdesc_sw128(v_addr + kk * C::KEYS_PER_PV_STEP * 128, C::ATOM_BYTES, 1024);
-          mma_ss<F32>(tmem + C::TM_O, ad, bd, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
+          mma_ts<F32>(d_tmem, p_tmem + kk * 8, bd, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
         }
-        mma_commit(&bar[B_VFREE0 + st]);
-        mma_commit(&bar[B_PDONE]);
       };
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const pi_work wk = p.work[w / p.units];
-        const int n = wk.n_ktiles;
+        const Unit u = get_unit(p, w);
+        const int n = u.wk.n_ktiles;
         mbar_wait(&bar[B_QFULL], item & 1);
+        mbar_wait(&bar[B_KFULL0 + (t % C::NS)], (t / C::NS) & 1);
         tc_fence_after();
-        for (int j = 0; j < n; ++j) {
-          const uint32_t tt = t + j;
-          const int st = tt % C::NS;
-          const int sb = tt & 1;
-          mbar_wait(&bar[B_KFULL0 + st], (tt / C::NS) & 1);
-          mbar_wait(&bar[B_SFREE0 + sb], ((tt >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t k_addr = sbase + C::OFF_K + st * C::TILE_BYTES;
-          const uint32_t d_tmem = tmem + (sb ? C::TM_S1 : C::TM_S0);
-#pragma unroll
-          for (int kk = 0; kk < C::QK_STEPS; ++kk) {
-            const uint32_t off = (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32;
-            mma_ss<F32>(d_tmem, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
-                        C::IDESC_QK, kk > 0 ? 1u : 0u);
+        if (u.has_b) {
+          // ---- pair unit: slot X keeps its S/P region X; ping-pong between the two tiles
+          issue_s(0, 0, t);
+          issue_s(1, 1, t);
+          mma_commit(&bar[B_KFREE0 + (t % C::NS)]);
+          if (n == 1) mma_commit(&bar[B_QFREE]);
+          for (int j = 0; j < n; ++j) {
+            const uint32_t tt = t + j;
+            for (int X = 0; X < 2; ++X) {
+              mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
+              if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
+              if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
+              tc_fence_after();
+              issue_pv(X, X, tt, j == 0);
+              if (X == 1) mma_commit(&bar[B_VFREE0 + (tt % C::NS)]);
+              if (j == n - 1) {
+                mma_commit(&bar[B_OFULL0 + X]);
+              } else {
+                if (X == 0) {
+                  mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NS)], ((tt + 1) / C::NS) & 1);
+                  tc_fence_after();
+                }
+                issue_s(X, X, tt + 1);
+                if (X == 1) {
+                  mma_commit(&bar[B_KFREE0 + ((tt + 1) % C::NS)]);
+                  if (j + 1 == n - 1) mma_commit(&bar[B_QFREE]);
+                }
+              }
+            }
           }
-          mma_commit(&bar[B_KFREE0 + st]);
-          mma_commit(&bar[B_SFULL0 + sb]);
-          if (j == n - 1) mma_commit(&bar[B_QFREE]);
-          if (j > 0) issue_pv(tt - 1, j == 1);
+          cnt[0] += n;
+          cnt[1] += n;
+          ix[0] += 1;
+          ix[1] += 1;
+        } else {
+          // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
+          issue_s(0, 0, t);
+          mma_commit(&bar[B_KFREE0 + (t % C::NS)]);
+          if (n > 1) {
+            mbar_wait(&bar[B_KFULL0 + ((t + 1) % C::NS)], ((t + 1) / C::NS) & 1);
+            tc_fence_after();
+            issue_s(0, 1, t + 1);
+            mma_commit(&bar[B_KFREE0 + ((t + 1) % C::NS)]);
+          }
+          if (n <= 2) mma_commit(&bar[B_QFREE]);
+          for (int j = 0; j < n; ++j) {
+            const uint32_t tt = t + j;
+            const int b = j & 1;
+            mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
+            mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
+            if (j == 0) mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
+            tc_fence_after();
+            issue_pv(0, b, tt, j == 0);
+            mma_commit(&bar[B_VFREE0 + (tt % C::NS)]);
+            if (j == n - 1) mma_commit(&bar[B_OFULL0]);
+            if (j + 2 < n) {
+              mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NS)], ((tt + 2) / C::NS) & 1);
+              tc_fence_after();
+              issue_s(0, b, tt + 2);
+              mma_commit(&bar[B_KFREE0 + ((tt + 2) % C::NS)]);
+              if (j + 2 == n - 1) mma_commit(&bar[B_QFREE]);
+            }
+          }
+          cnt[0] += (n + 1) >> 1;
+          cnt[1] += n >> 1;
+          ix[0] += 1;
         }
-        issue_pv(t + n - 1, n == 1);
         t += n;
         ++item;
       }
@@ -226,19 +307,21 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------------ Q gather
     constexpr int CH = C::ROW_BYTES / 16;  // 16-byte chunks per row
     uint32_t item = 0;
-    const uint32_t q_addr = sbase + C::OFF_Q;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const pi_work wk = p.work[w / p.units];
-      const int u = w % p.units;
+      const Unit u = get_unit(p, w);
+      const int nt = u.has_b ? 2 : 1;
       mbar_wait(&bar[B_QFREE], (item & 1) ^ 1);
-      const int n_chunks = wk.row_count * CH;
-      for (int idx = lane; idx < n_chunks; idx += 32) {
-        const int rr = idx / CH, c = idx % CH;
-        const pi_row row = p.rows[wk.row_begin + rr];
-        const int h = p.is_decode ? (u * p.r + (row.out & 15)) : u;
-        const uint8_t* src = p.q + ((int64_t)row.q_token * p.q_row_stride + (int64_t)h * D) * C::ES + c * 16;
-        const uint32_t dst = q_addr + (c >> 3) * C::ATOM_BYTES + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-        cp_async_16(dst, src);
+      const int n_chunks = u.wk.row_count * CH;
+      for (int X = 0; X < nt; ++X) {
+        const uint32_t q_addr = sbase + C::OFF_Q + X * C::TILE_BYTES;
+        for (int idx = lane; idx < n_chunks; idx += 32) {
+          const int rr = idx / CH, c = idx % CH;
+          const pi_row row = p.rows[u.wk.row_begin + rr];
+          const int h = u.head0 + X + (row.out & 15);
+          const uint8_t* src = p.q + ((int64_t)row.q_token * p.q_row_stride + (int64_t)h * D) * C::ES + c * 16;
+          const uint32_t dst = q_addr + (c >> 3) * C::ATOM_BYTES + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+          cp_async_16(dst, src);
+        }
       }
       cp_async_wait_all();
       fence_proxy_async_smem();
@@ -250,12 +333,10 @@ __global__ void __launch_bounds__(256, 1)
     if constexpr (F32) {
       uint32_t t = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const pi_work wk = p.work[w / p.units];
-        const int u = w % p.units;
-        const int kvh = p.is_decode ? u : u / p.r;
-        const float* vsrc = reinterpret_cast<const float*>(p.v_buf) + (int64_t)kvh * p.buffer_tokens * D;
-        for (int s = 0; s < wk.span_count; ++s) {
-          const pi_span sp = p.spans[wk.span_begin + s];
+        const Unit u = get_unit(p, w);
+        const float* vsrc = reinterpret_cast<const float*>(p.v_buf) + (int64_t)u.kvh * p.buffer_tokens * D;
+        for (int s = 0; s < u.wk.span_count; ++s) {
+          const pi_span sp = p.spans[u.wk.span_begin + s];
           for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
             const int st = t % C::NS;
             mbar_wait(&bar[B_VFREE0 + st], ((t / C::NS) & 1) ^ 1);
@@ -263,13 +344,15 @@ __global__ void __launch_bounds__(256, 1)
             for (int idx = lane; idx < 128 * (D / 4); idx += 32) {
               const int key = idx / (D / 4), c4 = idx % (D / 4);
               float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (k0 + key < p.buffer_tokens) v = *reinterpret_cast<const float4*>(vsrc + (int64_t)(k0 + key) * D + c4 * 4);
+              if (k0 + key < p.buffer_tokens)
+                v = *reinterpret_cast<const float4*>(vsrc + (int64_t)(k0 + key) * D + c4 * 4);
               const float ve[4] = {v.x, v.y, v.z, v.w};
               const int a = key >> 5, jj = (key & 31) >> 2, wb = (key & 3) * 4;
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int dch = c4 * 4 + e;
-                *reinterpret_cast<float*>(vt + a * C::VT_ATOM_BYTES + dch * 128 + ((jj ^ (dch & 7)) << 4) + wb) = ve[e];
+                *reinterpret_cast<float*>(vt + a * C::VT_ATOM_BYTES + dch * 128 + ((jj ^ (dch & 7)) << 4) + wb) =
+                    ve[e];
               }
             }
             fence_proxy_async_smem();
@@ -278,45 +361,42 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ------------------------------------------------------------------ softmax / epilogue
-    const int row_id = threadIdx.x - 128;  // == TMEM lane
-    const int wq = row_id >> 5;
+    const int X = (warp - 4) >> 2;         // tile slot: 0 = A (warps 4-7), 1 = B (warps 8-11)
+    const int row_id = (threadIdx.x - 128) & 127;
+    const int wq = row_id >> 5;            // == warp % 4: the TMEM lane quarter this warp may access
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const uint32_t p_gen_base = C::OFF_P;  // generic offset
-    uint32_t t = 0, item = 0;
+    const uint32_t o_tm = tmem + lane_base + (X ? C::TM_O1 : C::TM_O0);
+    uint32_t cnt[2] = {0, 0}, ix = 0, t = 0;
     const float NEG_INF = -INFINITY;
+    const float sl2 = p.scale_log2;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const pi_work wk = p.work[w / p.units];
-      const int u = w % p.units;
+      const Unit u = get_unit(p, w);
+      const pi_work& wk = u.wk;
+      const int n = wk.n_ktiles;
+      if (X == 1 && !u.has_b) {            // slot B idles; keep the region counters in step
+        cnt[0] += (n + 1) >> 1;
+        cnt[1] += n >> 1;
+        t += n;
+        continue;
+      }
       const bool valid = row_id < wk.row_count;
       const bool warp_any = wq * 32 < wk.row_count;
       pi_row row = {0, 0, 0, 0};
       if (valid) row = p.rows[wk.row_begin + row_id];
-      float m_ref = NEG_INF, l = 0.f, lr = 0.f;
+      float m_ref = NEG_INF, l = 0.f;
       uint32_t j = 0;
       for (int s = 0; s < wk.span_count; ++s) {
         const pi_span sp = p.spans[wk.span_begin + s];
         const bool last = (s == wk.span_count - 1);
         const int se = sp.begin + sp.len;
         for (int k0 = sp.begin; k0 < se; k0 += 128, ++j) {
-          const uint32_t tt = t + j;
-          const int sb = tt & 1;
-          mbar_wait(&bar[B_SFULL0 + sb], (tt >> 1) & 1);
+          const int b = u.has_b ? X : (int)(j & 1);          // S/P region of this tile
+          const uint32_t kb = u.has_b ? j : (j >> 1);        // use index of region b in this unit
+          const uint32_t s_tm = tmem + lane_base + (b ? C::TM_S1 : C::TM_S0);
+          mbar_wait(&bar[B_SFULL0 + b], (cnt[b] + kb) & 1);
           tc_fence_after();
-          uint32_t sr[128];
-          if (warp_any) {
-            const uint32_t sa = tmem + lane_base + (sb ? C::TM_S1 : C::TM_S0);
-            tmem_ld32(sa + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-            tmem_ld32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-            tmem_ld32(sa + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-            tmem_ld32(sa + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
-            tmem_wait_ld();
-            reg_fence(sr);
-          }
-          tc_fence_before();
-          mbar_arrive(&bar[B_SFREE0 + sb]);
-
           // visible key columns of this row in this tile: [c_lo, c_hi)
           int c_lo = 0, c_hi = 0;
           if (valid) {
@@ -328,111 +408,113 @@ __global__ void __launch_bounds__(256, 1)
             c_lo = lo_k - k0;
             c_hi = hi_k - k0;
           }
-          float mx = NEG_INF;
-          if (c_lo == 0 && c_hi == 128) {
+          if (warp_any) {
+            bool full = (c_lo == 0 && c_hi == 128);
+            // ---- pass 1: raw row max over the visible columns
+            float mx[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-              const float x = __uint_as_float(sr[c]) * p.scale_log2;
-              sr[c] = __float_as_uint(x);
-              mx = fmaxf(mx, x);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 128; ++c) {
-              const float x = (c >= c_lo && c < c_hi) ? __uint_as_float(sr[c]) * p.scale_log2 : NEG_INF;
-              sr[c] = __float_as_uint(x);
-              mx = fmaxf(mx, x);
-            }
-          }
-          const float m_new = fmaxf(m_ref, mx);
-          const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
-          if (warp_any && __any_sync(0xffffffffu, need)) {
-            // rescale O (TMEM) once the previous P.V has landed
-            mbar_wait(&bar[B_PDONE], (tt & 1) ^ 1);
-            tc_fence_after();
-            const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
-#pragma unroll
-            for (int c4 = 0; c4 < D / 32; ++c4) {
-              uint32_t o32[32];
-              const uint32_t oa = tmem + lane_base + C::TM_O + c4 * 32;
-              tmem_ld32(oa, o32);
+            for (int c4 = 0; c4 < 4; ++c4) {
+              uint32_t r[32];
+              tmem_ld32(s_tm + c4 * 32, r);
               tmem_wait_ld();
-              reg_fence(o32);
+              reg_fence(r);
+              if (full) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o32[i] = __float_as_uint(__uint_as_float(o32[i]) * alpha);
-              tmem_st32(oa, o32);
+                for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(r[i]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const int c = c4 * 32 + i;
+                  mx[i & 3] = fmaxf(mx[i & 3], (c >= c_lo && c < c_hi) ? __uint_as_float(r[i]) : NEG_INF);
+                }
+              }
             }
+            const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+            const float m_new = fmaxf(m_ref, mt * sl2);
+            const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
+            if (__any_sync(0xffffffffu, need)) {
+              if (!u.has_b && j > 0) {
+                // single-tile unit: P.V(j-1) may still be in flight; wait until it has landed
+                const uint32_t tp = t + j - 1;
+                mbar_wait(&bar[B_VFREE0 + (tp % C::NS)], (tp / C::NS) & 1);
+                tc_fence_after();
+              }
+              // (pair units: every earlier P.V of this slot completed before S(j) did)
+              const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
+#pragma unroll
+              for (int c4 = 0; c4 < D / 32; ++c4) {
+                uint32_t o32[32];
+                tmem_ld32(o_tm + c4 * 32, o32);
+                tmem_wait_ld();
+                reg_fence(o32);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o32[i] = __float_as_uint(__uint_as_float(o32[i]) * alpha);
+                tmem_st32(o_tm + c4 * 32, o32);
+              }
+              if (need) {
+                l *= alpha;
+                m_ref = m_new;
+              }
+            }
+            if (m_ref == NEG_INF) m_ref = m_new;
+            if (m_ref == NEG_INF) {              // nothing visible yet: P = 0 for this row
+              c_lo = c_hi = 0;
+              full = false;
+            }
+            // ---- pass 2: P = exp2(s * scale_log2 - m_ref), written over S in TMEM (branch-free)
+            const float nm = -m_ref;
+            float ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              uint32_t r[32];
+              tmem_ld32(s_tm + c4 * 32, r);
+              tmem_wait_ld();
+              reg_fence(r);
+              float pv[32];
+              if (full) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) pv[i] = ex2(fmaf(__uint_as_float(r[i]), sl2, nm));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const int c = c4 * 32 + i;
+                  const float x = fmaf(__uint_as_float(r[i]), sl2, nm);
+                  pv[i] = ex2((c >= c_lo && c < c_hi) ? x : NEG_INF);
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ps[i & 3] += pv[i];
+              if constexpr (!F32) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
+                tmem_st16(s_tm + c4 * 16, pk);
+              } else {
+                uint32_t pk[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(pv[i]);
+                tmem_st32(s_tm + c4 * 32, pk);
+              }
+            }
+            if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
             tmem_wait_st();
-            if (need) {
-              l *= alpha;
-              lr *= alpha;
-              m_ref = m_new;
-            }
           }
-          if (m_ref == NEG_INF) m_ref = m_new;
-
-          // P = exp2(x - m_ref) -> bf16 (tf32) into the swizzled K-major P tile
-          mbar_wait(&bar[B_PDONE], (tt & 1) ^ 1);  // previous P.V finished reading P
-          if (valid) {
-            const bool live = (m_ref != NEG_INF);
-            float psum = 0.f, prsum = 0.f;
-            uint8_t* prow = smem + p_gen_base + row_id * 128;
-            if constexpr (!F32) {
-#pragma unroll
-              for (int cc = 0; cc < 16; ++cc) {  // 8 keys per 16-byte chunk
-                uint32_t pk[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float a = live ? ex2(__uint_as_float(sr[cc * 8 + 2 * e]) - m_ref) : 0.f;
-                  const float b = live ? ex2(__uint_as_float(sr[cc * 8 + 2 * e + 1]) - m_ref) : 0.f;
-                  pk[e] = pack_bf16(a, b);
-                  psum += a + b;
-                  // O is normalised with the P the tensor core actually multiplies (bf16-rounded);
-                  // the LSE keeps the exact fp32 sum
-                  prsum += __uint_as_float(pk[e] << 16) + __uint_as_float(pk[e] & 0xffff0000u);
-                }
-                uint4* dst = reinterpret_cast<uint4*>(prow + (cc >> 3) * C::ATOM_BYTES +
-                                                      (((cc & 7) ^ (row_id & 7)) << 4));
-                *dst = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-              }
-            } else {
-#pragma unroll
-              for (int cc = 0; cc < 32; ++cc) {  // 4 keys per chunk
-                float pv[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  pv[e] = live ? ex2(__uint_as_float(sr[cc * 4 + e]) - m_ref) : 0.f;
-                  psum += pv[e];
-                  prsum += pv[e];
-                }
-                uint4* dst = reinterpret_cast<uint4*>(prow + (cc >> 3) * C::ATOM_BYTES +
-                                                      (((cc & 7) ^ (row_id & 7)) << 4));
-                *dst = make_uint4(__float_as_uint(pv[0]), __float_as_uint(pv[1]), __float_as_uint(pv[2]),
-                                  __float_as_uint(pv[3]));
-              }
-            }
-            l += psum;
-            lr += prsum;
-          }
-          fence_proxy_async_smem();
           tc_fence_before();
-          mbar_arrive(&bar[B_PFULL]);
+          mbar_arrive(&bar[B_PFULL0 + b]);
         }
       }
       // ---------------- epilogue: O / l -> out (or partial), lse
-      const uint32_t tlast = t + j - 1;
-      mbar_wait(&bar[B_PDONE], tlast & 1);
+      mbar_wait(&bar[B_OFULL0 + X], ix & 1);
       tc_fence_after();
-      const float inv_l = lr > 0.f ? 1.0f / lr : 0.f;
+      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
       const float lse_v = l > 0.f ? (m_ref + __log2f(l)) * 0.69314718055994530942f : NEG_INF;
       const int slot = (row.out >> 4) - 1;
-      const int hsub = row.out & 15;
-      const int head = p.is_decode ? (u * p.r + hsub) : u;
+      const int head = u.head0 + X + (row.out & 15);
       if (warp_any) {
 #pragma unroll
         for (int c4 = 0; c4 < D / 32; ++c4) {
           uint32_t o32[32];
-          tmem_ld32(tmem + lane_base + C::TM_O + c4 * 32, o32);
+          tmem_ld32(o_tm + c4 * 32, o32);
           tmem_wait_ld();
           reg_fence(o32);
           if (valid) {
@@ -468,7 +550,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bar[B_OFREE]);
+      mbar_arrive(&bar[B_OFREE0 + X]);
       if (valid) {
         if (slot < 0) {
           if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
@@ -476,8 +558,15 @@ __global__ void __launch_bounds__(256, 1)
           p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
         }
       }
-      t += j;
-      ++item;
+      if (u.has_b) {
+        cnt[0] += n;
+        cnt[1] += n;
+      } else {
+        cnt[0] += (n + 1) >> 1;
+        cnt[1] += n >> 1;
+      }
+      t += n;
+      ++ix;
     }
   }
   tc_fence_before();
@@ -501,7 +590,7 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
   p.rows = dp->rows;
   p.spans = dp->spans;
   p.n_work = n_work;
-  p.units = decode ? hkv_count : hkv_count * r;
+  p.units = decode ? hkv_count : hkv_count * ((r + 1) / 2);
   p.is_decode = decode ? 1 : 0;
   p.r = r;
   p.q = static_cast<const uint8_t*>(q);
@@ -538,7 +627,7 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
   }
   const int64_t total = (int64_t)n_work * p.units;
   const int grid = (int)std::min<int64_t>(total, num_sms());
-  packed_attention_kernel<D, F32><<<grid, 256, C::SMEM, stream>>>(p, tmK, tmV);
+  packed_attention_kernel<D, F32><<<grid, 384, C::SMEM, stream>>>(p, tmK, tmV);
   return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
 }
 
@@ -560,7 +649,8 @@ static pi_status attention_entry(bool decode, const pi_device_plan* dp, const vo
   const bool out_f32 = dt == PI_BF16_OUT_F32;
   if (out_f32) dt = PI_BF16;
   if (dt == PI_FP32 && head_dim != 64) return fail(PI_EUNSUP, "PI_FP32 supports head_dim 64 only");
-  if (q_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim || out_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim)
+  if (q_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim ||
+      out_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim)
     return fail(PI_EINVAL, "row stride smaller than the local heads");
   if (dp->n_partial_slots > 0 && decode && (!partial_o || !partial_lse))
     return fail(PI_EINVAL, "plan has split rows: partial_o / partial_lse required");
