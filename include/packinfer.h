@@ -30,7 +30,10 @@
  *                 [0, kv_len[i]) (a shared prefix's physical blocks first); row n + p maps
  *                 prefix p's tokens [0, prefix_len[p]).
  *   k/v_buf       [hkv_count, buffer_tokens, head_dim]  group-contiguous buffers B_g laid end
- *                 to end (base_g = sum of earlier group capacities)       (Alg. 1 Part 2)
+ *                 to end (base_g = sum of earlier group capacities)       (Alg. 1 Part 2).
+ *                 Internal workspace: for PI_BF16 caches k_buf holds bf16 (bitwise copies) and
+ *                 v_buf holds fp16 (exact conversion for |v| < 65504, saturated beyond), which
+ *                 lets the kernels multiply an fp16 P; for PI_FP32 both are fp32.
  *   partial_o     fp32 [n_partial_slots, hq_count, head_dim]; partial_lse fp32
  *                 [n_partial_slots, hq_count] — partial results of split rows (reading R10).
  */

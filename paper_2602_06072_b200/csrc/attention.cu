@@ -28,6 +28,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "device_common.h"
 #include "packinfer.h"
@@ -58,7 +59,20 @@ struct AttnParams {
   int32_t out_f32;         // 1: write out as fp32 (bf16 operands, fp32 output mode)
   const uint8_t* v_buf;    // fp32 path only: V staged transposed by warp 3
   int64_t buffer_tokens;
+  unsigned long long* trace;  // debug only (packinfer_debug_trace): CTA-0 clock64 timeline
+  int32_t q_heads_stride;  // q_row_stride / head_dim: rows of the 2D (token*stride + head, d) Q view
 };
+
+// Debug timeline: trace[(tile * 16 + event)], first TRACE_TILES tiles of CTA 0.
+constexpr int TRACE_TILES = 64;
+__device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int ev) {
+  if (p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
+    p.trace[tile * 16 + ev] = clock64();
+}
+// Per-unit events: trace[1024 + unit * 8 + ev], first 64 units of CTA 0.
+__device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
+  if (p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[1024 + unit * 8 + ev] = clock64();
+}
 
 template <int D, bool F32>
 struct AttnCfg {
@@ -81,9 +95,17 @@ struct AttnCfg {
   static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 128, 0, 0);
   // bf16: V is the MN-major B operand straight from TMA.  fp32 (kind::tf32): MN-major tf32 needs
   // the 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
-  static constexpr uint32_t IDESC_PV = idesc_make(FMT, 128, D, 0, F32 ? 0 : 1);
+  // P is stored as fp16 (10-bit mantissa: 8x smaller rounding than bf16; P <= 2^8 by the lazy
+  // rescale) and the relayout keeps V as fp16 in the group buffers: P.V is kind::f16 with f16 x f16.
+  static constexpr uint32_t IDESC_PV = F32 ? idesc_make(FMT, 128, D, 0, 0) : idesc_make2(0, 0, 128, D, 0, 1);
   static constexpr int VT_ATOM_BYTES = D * 128;       // fp32 V^T: D rows x 32 keys
   static constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
+  // warps 0..ROLE-1: TMA producer, MMA issuer, Q gather (+ V^T staging for fp32); then two softmax
+  // warpgroups of 4 warps.  A softmax warp may only touch TMEM lane quarter (warp % 4), and warps
+  // ROLE..ROLE+3 / ROLE+4..ROLE+7 each cover all four quarters.  Fewer role warps leave more
+  // registers per thread (65536 / THREADS) for the 128-column score row.
+  static constexpr int ROLE = 4;
+  static constexpr int THREADS = 32 * (ROLE + 8);
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -125,9 +147,9 @@ __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
 }
 
 template <int D, bool F32>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     packed_attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
-                            const __grid_constant__ CUtensorMap tmV) {
+                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ) {
   using C = AttnCfg<D, F32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -139,7 +161,7 @@ __global__ void __launch_bounds__(384, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[B_QFULL], 32);
+    mbar_init(&bar[B_QFULL], 1);
     mbar_init(&bar[B_QFREE], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar[B_KFULL0 + s], 1);
@@ -156,6 +178,7 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
+    prefetch_tmap(&tmQ);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -200,36 +223,45 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t t = 0, item = 0;
       uint32_t cnt[2] = {0, 0};   // completions so far of SFULL/PFULL of region 0 / 1
       uint32_t ix[2] = {0, 0};    // completions so far of OFULL/OFREE of slot 0 / 1
+      // Descriptors are built once; each k-step adds a compile-time offset to the 14-bit start
+      // address field (all smem offsets < 256 KB, so the field never carries).
+      const uint64_t dq = sdesc_sw128(sbase + C::OFF_Q, 16, 1024);
+      const uint64_t dk = sdesc_sw128(sbase + C::OFF_K, 16, 1024);
+      const uint64_t dv = F32 ? sdesc_sw128(sbase + C::OFF_V, 16, 1024)
+                              : sdesc_sw128(sbase + C::OFF_V, C::ATOM_BYTES, 1024);
+      constexpr uint64_t TILE16 = C::TILE_BYTES >> 4;
       // S(X) = Q_X K(tt)^T into S/P region b
       auto issue_s = [&](int X, int b, uint32_t tt) {
-        const uint32_t q_addr = sbase + C::OFF_Q + X * C::TILE_BYTES;
-        const uint32_t k_addr = sbase + C::OFF_K + (tt % C::NS) * C::TILE_BYTES;
+        const uint64_t aq = dq + X * TILE16;
+        const uint64_t bk = dk + (tt % C::NS) * TILE16;
         const uint32_t d_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
 #pragma unroll
         for (int kk = 0; kk < C::QK_STEPS; ++kk) {
-          const uint32_t off = (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32;
-          mma_ss<F32>(d_tmem, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
-                      C::IDESC_QK, kk > 0 ? 1u : 0u);
+          const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
+          mma_ss<F32>(d_tmem, aq + off, bk + off, C::IDESC_QK, kk > 0 ? 1u : 0u);
         }
         mma_commit(&bar[B_SFULL0 + b]);
       };
       // O_X += P(region b) V(tt)
       auto issue_pv = [&](int X, int b, uint32_t tt, bool first) {
-        const uint32_t v_addr = sbase + C::OFF_V + (tt % C::NS) * C::TILE_BYTES;
+        const uint64_t bv = dv + (tt % C::NS) * TILE16;
         const uint32_t p_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
         const uint32_t d_tmem = tmem + (X ? C::TM_O1 : C::TM_O0);
 #pragma unroll
         for (int kk = 0; kk < C::PV_STEPS; ++kk) {
-          const uint64_t bd = F32 ? sdesc_sw128(v_addr + (kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32, 16, 1024)
-                                  : sdesc_sw128(v_addr + kk * C::KEYS_PER_PV_STEP * 128, C::ATOM_BYTES, 1024);
-          mma_ts<F32>(d_tmem, p_tmem + kk * 8, bd, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
+          const uint64_t off = F32 ? (uint64_t)(((kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32) >> 4)
+                                   : (uint64_t)((kk * C::KEYS_PER_PV_STEP * 128) >> 4);
+          mma_ts<F32>(d_tmem, p_tmem + kk * 8, bv + off, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
         }
       };
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         const Unit u = get_unit(p, w);
         const int n = u.wk.n_ktiles;
+        trace_unit(p, item, 0);
         mbar_wait(&bar[B_QFULL], item & 1);
+        trace_unit(p, item, 1);
         mbar_wait(&bar[B_KFULL0 + (t % C::NS)], (t / C::NS) & 1);
+        trace_unit(p, item, 2);
         tc_fence_after();
         if (u.has_b) {
           // ---- pair unit: slot X keeps its S/P region X; ping-pong between the two tiles
@@ -240,11 +272,14 @@ __global__ void __launch_bounds__(384, 1)
           for (int j = 0; j < n; ++j) {
             const uint32_t tt = t + j;
             for (int X = 0; X < 2; ++X) {
+              trace_ev(p, tt, 0 + 3 * X);
               mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
+              trace_ev(p, tt, 1 + 3 * X);
               if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
               if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
               tc_fence_after();
               issue_pv(X, X, tt, j == 0);
+              trace_ev(p, tt, 14 + X);
               if (X == 1) mma_commit(&bar[B_VFREE0 + (tt % C::NS)]);
               if (j == n - 1) {
                 mma_commit(&bar[B_OFULL0 + X]);
@@ -254,6 +289,7 @@ __global__ void __launch_bounds__(384, 1)
                   tc_fence_after();
                 }
                 issue_s(X, X, tt + 1);
+                trace_ev(p, tt, 2 + 3 * X);
                 if (X == 1) {
                   mma_commit(&bar[B_KFREE0 + ((tt + 1) % C::NS)]);
                   if (j + 1 == n - 1) mma_commit(&bar[B_QFREE]);
@@ -298,37 +334,46 @@ __global__ void __launch_bounds__(384, 1)
           cnt[1] += n >> 1;
           ix[0] += 1;
         }
+        trace_unit(p, item, 3);
         t += n;
         ++item;
       }
     }
     __syncwarp();
   } else if (warp == 2) {
-    // ------------------------------------------------------------------ Q gather
-    constexpr int CH = C::ROW_BYTES / 16;  // 16-byte chunks per row
+    // ------------------------------------------------------------------ Q gather (TMA tile::gather4)
+    // Q rows are addressed through the plan's row table: lane g gathers rows 4g..4g+3 of each tile
+    // (one gather4 per 128-byte atom column) straight into the SWIZZLE_128B K-major operand layout.
     uint32_t item = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       const Unit u = get_unit(p, w);
       const int nt = u.has_b ? 2 : 1;
+      trace_unit(p, item, 4);
       mbar_wait(&bar[B_QFREE], (item & 1) ^ 1);
-      const int n_chunks = u.wk.row_count * CH;
-      for (int X = 0; X < nt; ++X) {
-        const uint32_t q_addr = sbase + C::OFF_Q + X * C::TILE_BYTES;
-        for (int idx = lane; idx < n_chunks; idx += 32) {
-          const int rr = idx / CH, c = idx % CH;
-          const pi_row row = p.rows[u.wk.row_begin + rr];
-          const int h = u.head0 + X + (row.out & 15);
-          const uint8_t* src = p.q + ((int64_t)row.q_token * p.q_row_stride + (int64_t)h * D) * C::ES + c * 16;
-          const uint32_t dst = q_addr + (c >> 3) * C::ATOM_BYTES + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-          cp_async_16(dst, src);
+      trace_unit(p, item, 5);
+      const int rows = u.wk.row_count;
+      const int groups = (rows + 3) >> 2;
+      if (lane == 0) mbar_arrive_expect_tx(&bar[B_QFULL], (uint32_t)(nt * groups * C::ATOMS * 512));
+      __syncwarp();
+      if (lane < groups) {
+        int32_t ri[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const pi_row row = p.rows[u.wk.row_begin + min(4 * lane + e, rows - 1)];
+          ri[e] = row.q_token * p.q_heads_stride + u.head0 + (row.out & 15);
+        }
+        for (int X = 0; X < nt; ++X) {
+          uint8_t* dst = smem + C::OFF_Q + X * C::TILE_BYTES + lane * 512;
+#pragma unroll
+          for (int a = 0; a < C::ATOMS; ++a)
+            tma_gather4(dst + a * C::ATOM_BYTES, &tmQ, &bar[B_QFULL], a * C::ATOM_ELEMS, ri[0] + X, ri[1] + X,
+                        ri[2] + X, ri[3] + X);
         }
       }
-      cp_async_wait_all();
-      fence_proxy_async_smem();
-      mbar_arrive(&bar[B_QFULL]);
+      if (lane == 0) trace_unit(p, item, 6);
       ++item;
     }
-  } else if (warp == 3) {
+  } else if (warp < C::ROLE) {
     // ------------------------------------------------------------------ fp32 only: V^T staging
     if constexpr (F32) {
       uint32_t t = 0;
@@ -363,9 +408,9 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else {
     // ------------------------------------------------------------------ softmax / epilogue
-    const int X = (warp - 4) >> 2;         // tile slot: 0 = A (warps 4-7), 1 = B (warps 8-11)
-    const int row_id = (threadIdx.x - 128) & 127;
-    const int wq = row_id >> 5;            // == warp % 4: the TMEM lane quarter this warp may access
+    const int X = (warp - C::ROLE) >> 2;   // tile slot: 0 = A, 1 = B
+    const int wq = warp & 3;               // the TMEM lane quarter this warp may access
+    const int row_id = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t o_tm = tmem + lane_base + (X ? C::TM_O1 : C::TM_O0);
     uint32_t cnt[2] = {0, 0}, ix = 0, t = 0;
@@ -395,8 +440,10 @@ __global__ void __launch_bounds__(384, 1)
           const int b = u.has_b ? X : (int)(j & 1);          // S/P region of this tile
           const uint32_t kb = u.has_b ? j : (j >> 1);        // use index of region b in this unit
           const uint32_t s_tm = tmem + lane_base + (b ? C::TM_S1 : C::TM_S0);
+          if (row_id == 0) trace_ev(p, t + j, 6 + 4 * X);
           mbar_wait(&bar[B_SFULL0 + b], (cnt[b] + kb) & 1);
           tc_fence_after();
+          if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
           // visible key columns of this row in this tile: [c_lo, c_hi)
           int c_lo = 0, c_hi = 0;
           if (valid) {
@@ -409,30 +456,108 @@ __global__ void __launch_bounds__(384, 1)
             c_hi = hi_k - k0;
           }
           if (warp_any) {
-            bool full = (c_lo == 0 && c_hi == 128);
-            // ---- pass 1: raw row max over the visible columns
-            float mx[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
+            const bool full = (c_lo == 0 && c_hi == 128);
+            // Streaming single pass over two 64-column halves: each S element is read from TMEM
+            // once.  The running max is updated per half (lazily: only when it grows by > 2^8);
+            // if the second half raises it, the first half's P (already in TMEM) and O are rescaled.
+            float ps[4] = {0.f, 0.f, 0.f, 0.f};
+            float alpha_o = 1.0f;     // pending O rescale for this tile
+            bool any_o = false;
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              uint32_t r[32];
-              tmem_ld32(s_tm + c4 * 32, r);
+            for (int h = 0; h < 2; ++h) {
+              uint32_t r[64];
+              tmem_ld32(s_tm + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              tmem_ld32(s_tm + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
               tmem_wait_ld();
               reg_fence(r);
-              if (full) {
+              if (!full) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(r[i]));
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const int c = c4 * 32 + i;
-                  mx[i & 3] = fmaxf(mx[i & 3], (c >= c_lo && c < c_hi) ? __uint_as_float(r[i]) : NEG_INF);
+                for (int i = 0; i < 64; ++i) {
+                  const int c = h * 64 + i;
+                  if (!(c >= c_lo && c < c_hi)) r[i] = __float_as_uint(NEG_INF);
                 }
               }
+              float mx[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
+#pragma unroll
+              for (int i = 0; i < 64; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(r[i]));
+              const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+              const float m_new = fmaxf(m_ref, mt * sl2);
+              const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
+              if (__any_sync(0xffffffffu, need)) {
+                const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
+                if (h == 1) {
+                  // P of the first half was exponentiated against the old max
+#pragma unroll
+                  for (int c = 0; c < (F32 ? 64 : 32); c += 32) {
+                    uint32_t q32[32];
+                    tmem_ld32(s_tm + c, q32);
+                    tmem_wait_ld();
+                    reg_fence(q32);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                      q32[i] = F32 ? __float_as_uint(__uint_as_float(q32[i]) * alpha)
+                                   : pack_f16(__half2float(__ushort_as_half((unsigned short)(q32[i] & 0xffffu))) * alpha,
+                                              __half2float(__ushort_as_half((unsigned short)(q32[i] >> 16))) * alpha);
+                    tmem_st32(s_tm + c, q32);
+                  }
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) ps[k] *= alpha;
+                }
+                alpha_o *= alpha;
+                any_o = true;
+                if (need) {
+                  l *= alpha;
+                  m_ref = m_new;
+                }
+              }
+              if (m_ref == NEG_INF) m_ref = m_new;
+              // P = exp2(s * scale_log2 - m_ref): FFMA2 for the argument, 3 of 8 pairs on the FMA
+              // pipe (ex2_poly2), the rest on MUFU; masked columns hold -inf -> 0
+              const bool live = m_ref != NEG_INF;
+              const float nm = live ? -m_ref : NEG_INF;
+              const uint64_t SL2 = f2(sl2, sl2), NM = f2(nm, nm);
+              uint64_t acc0 = f2(ps[0], ps[1]), acc1 = f2(ps[2], ps[3]);
+              // two branch-free bodies: full tiles offload 3 of 8 pairs to the FMA pipe
+              auto body = [&](auto use_poly) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const uint64_t x =
+                      f2_fma(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), SL2, NM);
+                  uint64_t e;
+                  if (decltype(use_poly)::value && (i & 7) >= 5)
+                    e = ex2_poly2(x);
+                  else
+                    e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
+                  if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
+                  if constexpr (!F32) {
+                    r[i] = pack_f16(f2_lo(e), f2_hi(e));      // in place: i <= 2i
+                  } else {
+                    r[2 * i] = __float_as_uint(f2_lo(e));
+                    r[2 * i + 1] = __float_as_uint(f2_hi(e));
+                  }
+                }
+              };
+              if (!F32 && full)
+                body(std::true_type{});
+              else
+                body(std::false_type{});
+              ps[0] = f2_lo(acc0);
+              ps[1] = f2_hi(acc0);
+              ps[2] = f2_lo(acc1);
+              ps[3] = f2_hi(acc1);
+              if constexpr (!F32) {
+                tmem_st32(s_tm + h * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              } else {
+                tmem_st32(s_tm + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+                tmem_st32(s_tm + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+              }
             }
-            const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-            const float m_new = fmaxf(m_ref, mt * sl2);
-            const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
-            if (__any_sync(0xffffffffu, need)) {
+            if (row_id == 0) trace_ev(p, t + j, 8 + 4 * X);
+            const bool any_need = any_o && j > 0;   // tile 0 overwrites O (accumulate = 0)
+            const float alpha = alpha_o;
+            if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+            // ---- lazy O rescale (rare): before P(j) is released to the tensor core
+            if (any_need) {
               if (!u.has_b && j > 0) {
                 // single-tile unit: P.V(j-1) may still be in flight; wait until it has landed
                 const uint32_t tp = t + j - 1;
@@ -440,7 +565,6 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
               }
               // (pair units: every earlier P.V of this slot completed before S(j) did)
-              const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
 #pragma unroll
               for (int c4 = 0; c4 < D / 32; ++c4) {
                 uint32_t o32[32];
@@ -451,56 +575,12 @@ __global__ void __launch_bounds__(384, 1)
                 for (int i = 0; i < 32; ++i) o32[i] = __float_as_uint(__uint_as_float(o32[i]) * alpha);
                 tmem_st32(o_tm + c4 * 32, o32);
               }
-              if (need) {
-                l *= alpha;
-                m_ref = m_new;
-              }
             }
-            if (m_ref == NEG_INF) m_ref = m_new;
-            if (m_ref == NEG_INF) {              // nothing visible yet: P = 0 for this row
-              c_lo = c_hi = 0;
-              full = false;
-            }
-            // ---- pass 2: P = exp2(s * scale_log2 - m_ref), written over S in TMEM (branch-free)
-            const float nm = -m_ref;
-            float ps[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              uint32_t r[32];
-              tmem_ld32(s_tm + c4 * 32, r);
-              tmem_wait_ld();
-              reg_fence(r);
-              float pv[32];
-              if (full) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) pv[i] = ex2(fmaf(__uint_as_float(r[i]), sl2, nm));
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const int c = c4 * 32 + i;
-                  const float x = fmaf(__uint_as_float(r[i]), sl2, nm);
-                  pv[i] = ex2((c >= c_lo && c < c_hi) ? x : NEG_INF);
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 32; ++i) ps[i & 3] += pv[i];
-              if constexpr (!F32) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
-                tmem_st16(s_tm + c4 * 16, pk);
-              } else {
-                uint32_t pk[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(pv[i]);
-                tmem_st32(s_tm + c4 * 32, pk);
-              }
-            }
-            if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
             tmem_wait_st();
           }
           tc_fence_before();
           mbar_arrive(&bar[B_PFULL0 + b]);
+          if (row_id == 0) trace_ev(p, t + j, 9 + 4 * X);
         }
       }
       // ---------------- epilogue: O / l -> out (or partial), lse
@@ -577,6 +657,8 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+unsigned long long* g_debug_trace = nullptr;
+
 template <int D, bool F32>
 static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, const void* q, int64_t q_row_stride,
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
@@ -606,6 +688,7 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
   p.v_buf = static_cast<const uint8_t*>(v_buf);
   p.out_f32 = out_f32 ? 1 : 0;
   p.buffer_tokens = dp->buffer_tokens;
+  p.trace = g_debug_trace;
 
   CUtensorMap tmK, tmV;
   const CUtensorMapDataType dt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -614,7 +697,16 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
   const uint32_t box[3] = {(uint32_t)C::ATOM_ELEMS, 128u, 1u};
   pi_status s = encode_tmap_3d(&tmK, dt, k_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
-  s = encode_tmap_3d(&tmV, dt, v_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  s = encode_tmap_3d(&tmV, F32 ? dt : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, v_buf, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+  if (s != PI_OK) return s;
+  // Q as a 2D (row = token * q_heads_stride + head, d) tensor for tile::gather4 (box {atom, 1})
+  CUtensorMap tmQ;
+  p.q_heads_stride = (int32_t)(q_row_stride / D);
+  const uint64_t qdims[3] = {(uint64_t)D, (uint64_t)dp->total_q * (uint64_t)p.q_heads_stride, 1};
+  const uint64_t qstrides[2] = {(uint64_t)C::ROW_BYTES, (uint64_t)dp->total_q * p.q_heads_stride * C::ROW_BYTES};
+  const uint32_t qbox[3] = {(uint32_t)C::ATOM_ELEMS, 1u, 1u};
+  s = encode_tmap_2d(&tmQ, dt, q, qdims, qstrides, qbox, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
 
   static bool attr_set = false;  // per template instance
@@ -627,7 +719,7 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
   }
   const int64_t total = (int64_t)n_work * p.units;
   const int grid = (int)std::min<int64_t>(total, num_sms());
-  packed_attention_kernel<D, F32><<<grid, 384, C::SMEM, stream>>>(p, tmK, tmV);
+  packed_attention_kernel<D, F32><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ);
   return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
 }
 
@@ -649,6 +741,7 @@ static pi_status attention_entry(bool decode, const pi_device_plan* dp, const vo
   const bool out_f32 = dt == PI_BF16_OUT_F32;
   if (out_f32) dt = PI_BF16;
   if (dt == PI_FP32 && head_dim != 64) return fail(PI_EUNSUP, "PI_FP32 supports head_dim 64 only");
+  if (q_row_stride % head_dim) return fail(PI_EINVAL, "q_row_stride must be a multiple of head_dim");
   if (q_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim ||
       out_row_stride < (int64_t)hkv_count * gqa_ratio * head_dim)
     return fail(PI_EINVAL, "row stride smaller than the local heads");
@@ -676,6 +769,10 @@ static pi_status attention_entry(bool decode, const pi_device_plan* dp, const vo
 }  // namespace pi
 
 extern "C" {
+
+// Debug hook (not part of the ABI header): device buffer of >= 64*16 uint64 that the next attention
+// launches fill with CTA 0's clock64 timeline; NULL disables.
+PI_API void packinfer_debug_trace(void* dev_buf) { pi::g_debug_trace = static_cast<unsigned long long*>(dev_buf); }
 
 pi_status packinfer_attention_prefill(const pi_device_plan* dp, const void* q, int64_t q_row_stride,
                                       const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,

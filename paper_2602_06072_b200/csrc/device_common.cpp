@@ -12,9 +12,9 @@ EncodeFn g_encode = nullptr;
 std::once_flag g_encode_once;
 }  // namespace
 
-pi_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
-                         const uint64_t dims[3], const uint64_t strides_bytes[2], const uint32_t box[3],
-                         CUtensorMapSwizzle swizzle) {
+static pi_status encode_tmap(int rank, CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
+                             const uint64_t dims[3], const uint64_t strides_bytes[2], const uint32_t box[3],
+                             CUtensorMapSwizzle swizzle) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -27,11 +27,23 @@ pi_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void
   cuuint64_t gs[2] = {strides_bytes[0], strides_bytes[1]};
   cuuint32_t bd[3] = {box[0], box[1], box[2]};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_encode(map, dtype, 3, const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  CUresult r = g_encode(map, dtype, rank, const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(PI_ECUDA, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
   return PI_OK;
+}
+
+pi_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
+                         const uint64_t dims[3], const uint64_t strides_bytes[2], const uint32_t box[3],
+                         CUtensorMapSwizzle swizzle) {
+  return encode_tmap(3, map, dtype, base, dims, strides_bytes, box, swizzle);
+}
+
+pi_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
+                         const uint64_t dims[3], const uint64_t strides_bytes[2], const uint32_t box[3],
+                         CUtensorMapSwizzle swizzle) {
+  return encode_tmap(2, map, dtype, base, dims, strides_bytes, box, swizzle);
 }
 
 int num_sms() {

@@ -17,6 +17,11 @@ pi_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void
                          const uint64_t dims[3], const uint64_t strides_bytes[2],
                          const uint32_t box[3], CUtensorMapSwizzle swizzle);
 
+// Rank-2 variant (dims[2] / strides[1] / box[2] ignored).
+pi_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
+                         const uint64_t dims[3], const uint64_t strides_bytes[2],
+                         const uint32_t box[3], CUtensorMapSwizzle swizzle);
+
 // Number of SMs of the current device (cached per device).
 int num_sms();
 

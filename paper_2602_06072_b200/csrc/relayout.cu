@@ -1,12 +1,15 @@
 // Contiguous memory consolidation (PackInfer §3.2; Alg. 1 Copy lines P:244/P:250).
 //
 // Gathers every copy-plan entry from the paged KV cache [num_blocks, page, Hkv, d] into the
-// group-contiguous buffers [hkv_count, buffer_tokens, d].  One warp per buffer token: it reads
+// group-contiguous buffers [hkv_count, buffer_tokens, d].  For bf16 caches V is stored as fp16
+// (exact for |v| < 65504, saturated beyond) so that the packed attention can multiply an fp16 P
+// (8x finer than bf16) with it; K is copied bitwise.  One warp per buffer token: it reads
 // the token's hkv_count*d contiguous elements (all local heads of one paged slot: coalesced) and
 // scatters them into the per-head buffers.  Cells in a suffix's headroom (delta) are
 // written with zeros so every buffer cell is finite (the attention kernels read whole 128-key
 // tiles; masked keys meet P = 0, which must not multiply NaN garbage).
 // HBM-bound: algorithmic bytes = 2 (K,V) x copied tokens x hkv_count x d x elem (read + write).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,7 +37,20 @@ struct RelayoutParams {
   int64_t buf_head_bytes;     // buffer_tokens * d * es
   uint8_t* kb;
   uint8_t* vb;
+  int32_t v_to_f16;           // bf16 caches: convert V to fp16 on the way
 };
+
+__device__ __forceinline__ uint4 bf16x8_to_f16x8(uint4 v) {
+  uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = fminf(fmaxf(__uint_as_float(w[i] << 16), -65504.f), 65504.f);
+    const float hi = fminf(fmaxf(__uint_as_float(w[i] & 0xffff0000u), -65504.f), 65504.f);
+    __half2 h = __floats2half2_rn(lo, hi);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
 
 __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
   const int64_t g = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -73,7 +89,7 @@ __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
           const int h = i / p.head_chunks, c = i % p.head_chunks;
           const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)c * 16;
           *reinterpret_cast<uint4*>(p.kb + d) = kv[u];
-          *reinterpret_cast<uint4*>(p.vb + d) = vv[u];
+          *reinterpret_cast<uint4*>(p.vb + d) = p.v_to_f16 ? bf16x8_to_f16x8(vv[u]) : vv[u];
         }
       }
     }
@@ -126,6 +142,7 @@ extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void*
   p.buf_head_bytes = dp->buffer_tokens * head_dim * es;
   p.kb = static_cast<uint8_t*>(k_buf);
   p.vb = static_cast<uint8_t*>(v_buf);
+  p.v_to_f16 = dt == PI_BF16 ? 1 : 0;
   const int64_t blocks = (p.total + 7) / 8;
   if (blocks > 0x7fffffff) return fail(PI_EINVAL, "buffer too large");
   relayout_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace pi {
 namespace sm100 {
@@ -70,6 +71,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// Gather 4 rows (arbitrary row coordinates r0..r3, column c0) of a 2D tensor map into 4 consecutive
+// 128-byte smem rows (box {cols, 1}); the 128B swizzle follows the destination address.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t r0,
+                                            int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
 
@@ -200,6 +212,62 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// Instruction descriptor with separate A / B formats (kind::f16: 0 = f16, 1 = bf16).
+__host__ __device__ constexpr uint32_t idesc_make2(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N,
+                                                   uint32_t a_mn_major, uint32_t b_mn_major) {
+  return (1u << 4) | (a_fmt << 7) | (b_fmt << 10) | (a_mn_major << 15) | (b_mn_major << 16) |
+         ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------------------- packed fp32x2
+// sm_100 FFMA2 / FADD2: two fp32 lanes per instruction (register pairs).
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float f2_hi(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (MUFU offload): x clamped to >= -125, x = n + f with
+// n = rint(x) (1.5*2^23 magic add), f in [-1/2, 1/2], 2^f by a minimax cubic (max rel. err
+// 7.5e-5, well below the bf16 rounding P receives), then n is added to the exponent field.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
+  const float MAGIC = 12582912.0f;
+  const uint64_t xc = f2(fmaxf(f2_lo(x), -125.0f), fmaxf(f2_hi(x), -125.0f));
+  const uint64_t t = f2_add(xc, f2(MAGIC, MAGIC));
+  const uint64_t n = f2_add(t, f2(-MAGIC, -MAGIC));
+  const uint64_t f = f2_fma(n, f2(-1.0f, -1.0f), xc);
+  uint64_t p = f2_fma(f, f2(0.0551710967f, 0.0551710967f), f2(0.2426099964f, 0.2426099964f));
+  p = f2_fma(p, f, f2(0.6932609731f, 0.6932609731f));
+  p = f2_fma(p, f, f2(0.9999281437f, 0.9999281437f));
+  const uint32_t tl = __float_as_uint(f2_lo(t)), th = __float_as_uint(f2_hi(t));
+  const uint32_t lo = __float_as_uint(f2_lo(p)) + (tl << 23);
+  const uint32_t hi = __float_as_uint(f2_hi(p)) + (th << 23);
+  return f2(__uint_as_float(lo), __uint_as_float(hi));
 }
 
 }  // namespace sm100

@@ -307,7 +307,9 @@ class PackedBatch:
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena)
         bt = max(int(c.buffer_tokens), 1)
         self.k_buf = torch.empty((hkv_count, bt, head_dim), dtype=dtype, device=self.device)
-        self.v_buf = torch.empty_like(self.k_buf)
+        # bf16 caches keep V as fp16 in the group buffer (include/packinfer.h)
+        self.v_buf = torch.empty((hkv_count, bt, head_dim), dtype=torch.float16 if dtype == torch.bfloat16 else dtype,
+                                 device=self.device)
         hq = hkv_count * gqa_ratio
         ns = max(int(c.n_partial_slots), 1)
         self.partial_o = torch.empty((ns, hq, head_dim), dtype=torch.float32, device=self.device)
