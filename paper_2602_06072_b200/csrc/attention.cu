@@ -63,15 +63,15 @@ struct AttnParams {
   int32_t q_heads_stride;  // q_row_stride / head_dim: rows of the 2D (token*stride + head, d) Q view
 };
 
-// Debug timeline: trace[(tile * 16 + event)], first TRACE_TILES tiles of CTA 0.
+// Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
 constexpr int TRACE_TILES = 64;
 __device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int ev) {
   if (p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
-    p.trace[tile * 16 + ev] = clock64();
+    p.trace[tile * 24 + ev] = clock64();
 }
 // Per-unit events: trace[1024 + unit * 8 + ev], first 64 units of CTA 0.
 __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
-  if (p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[1024 + unit * 8 + ev] = clock64();
+  if (p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[64 * 24 + unit * 8 + ev] = clock64();
 }
 
 template <int D, bool F32>
@@ -189,37 +189,43 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t t = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const Unit u = get_unit(p, w);
-        for (int s = 0; s < u.wk.span_count; ++s) {
-          const pi_span sp = p.spans[u.wk.span_begin + s];
-          for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
-            const int st = t % C::NS;
-            const uint32_t ph = (t / C::NS) & 1;
-            mbar_wait(&bar[B_KFREE0 + st], ph ^ 1);
+    // The whole warp walks the schedule (uniform values); one elected lane issues each copy.
+    uint32_t t = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const Unit u = get_unit(p, w);
+      for (int s = 0; s < u.wk.span_count; ++s) {
+        const pi_span sp = p.spans[u.wk.span_begin + s];
+        for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
+          const int st = t % C::NS;
+          const uint32_t ph = (t / C::NS) & 1;
+          mbar_wait(&bar[B_KFREE0 + st], ph ^ 1);
+          if (elect_one()) {
             mbar_arrive_expect_tx(&bar[B_KFULL0 + st], C::TILE_BYTES);
 #pragma unroll
             for (int a = 0; a < C::ATOMS; ++a)
               tma_load_3d(smem + C::OFF_K + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmK, &bar[B_KFULL0 + st],
                           a * C::ATOM_ELEMS, k0, u.kvh);
-            if constexpr (!F32) {
-              mbar_wait(&bar[B_VFREE0 + st], ph ^ 1);
+          }
+          __syncwarp();
+          if constexpr (!F32) {
+            mbar_wait(&bar[B_VFREE0 + st], ph ^ 1);
+            if (elect_one()) {
               mbar_arrive_expect_tx(&bar[B_VFULL0 + st], C::TILE_BYTES);
 #pragma unroll
               for (int a = 0; a < C::ATOMS; ++a)
                 tma_load_3d(smem + C::OFF_V + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmV, &bar[B_VFULL0 + st],
                             a * C::ATOM_ELEMS, k0, u.kvh);
             }
+            __syncwarp();
           }
         }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // The whole warp walks the schedule with warp-uniform values (uniform registers); each batch of
+    // tcgen05.mma / commit is issued by one elected lane (no per-MMA waterfall loops).
+    {
       uint32_t t = 0, item = 0;
       uint32_t cnt[2] = {0, 0};   // completions so far of SFULL/PFULL of region 0 / 1
       uint32_t ix[2] = {0, 0};    // completions so far of OFULL/OFREE of slot 0 / 1
@@ -235,24 +241,34 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         const uint64_t aq = dq + X * TILE16;
         const uint64_t bk = dk + (tt % C::NS) * TILE16;
         const uint32_t d_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < C::QK_STEPS; ++kk) {
-          const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
-          mma_ss<F32>(d_tmem, aq + off, bk + off, C::IDESC_QK, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < C::QK_STEPS; ++kk) {
+            const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
+            mma_ss<F32>(d_tmem, aq + off, bk + off, C::IDESC_QK, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bar[B_SFULL0 + b]);
         }
-        mma_commit(&bar[B_SFULL0 + b]);
+        __syncwarp();
+      };
+      auto commit = [&](int id) {
+        if (elect_one()) mma_commit(&bar[id]);
+        __syncwarp();
       };
       // O_X += P(region b) V(tt)
       auto issue_pv = [&](int X, int b, uint32_t tt, bool first) {
         const uint64_t bv = dv + (tt % C::NS) * TILE16;
         const uint32_t p_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
         const uint32_t d_tmem = tmem + (X ? C::TM_O1 : C::TM_O0);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < C::PV_STEPS; ++kk) {
-          const uint64_t off = F32 ? (uint64_t)(((kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32) >> 4)
-                                   : (uint64_t)((kk * C::KEYS_PER_PV_STEP * 128) >> 4);
-          mma_ts<F32>(d_tmem, p_tmem + kk * 8, bv + off, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
+          for (int kk = 0; kk < C::PV_STEPS; ++kk) {
+            const uint64_t off = F32 ? (uint64_t)(((kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32) >> 4)
+                                     : (uint64_t)((kk * C::KEYS_PER_PV_STEP * 128) >> 4);
+            mma_ts<F32>(d_tmem, p_tmem + kk * 8, bv + off, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
+          }
         }
+        __syncwarp();
       };
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         const Unit u = get_unit(p, w);
@@ -267,8 +283,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           // ---- pair unit: slot X keeps its S/P region X; ping-pong between the two tiles
           issue_s(0, 0, t);
           issue_s(1, 1, t);
-          mma_commit(&bar[B_KFREE0 + (t % C::NS)]);
-          if (n == 1) mma_commit(&bar[B_QFREE]);
+          commit(B_KFREE0 + (t % C::NS));
+          if (n == 1) commit(B_QFREE);
           for (int j = 0; j < n; ++j) {
             const uint32_t tt = t + j;
             for (int X = 0; X < 2; ++X) {
@@ -277,22 +293,24 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               trace_ev(p, tt, 1 + 3 * X);
               if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
               if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
+              trace_ev(p, tt, 16 + X);
               tc_fence_after();
               issue_pv(X, X, tt, j == 0);
               trace_ev(p, tt, 14 + X);
-              if (X == 1) mma_commit(&bar[B_VFREE0 + (tt % C::NS)]);
+              if (X == 1) commit(B_VFREE0 + (tt % C::NS));
               if (j == n - 1) {
-                mma_commit(&bar[B_OFULL0 + X]);
+                commit(B_OFULL0 + X);
               } else {
                 if (X == 0) {
                   mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NS)], ((tt + 1) / C::NS) & 1);
                   tc_fence_after();
                 }
+                trace_ev(p, tt, 18 + X);
                 issue_s(X, X, tt + 1);
                 trace_ev(p, tt, 2 + 3 * X);
                 if (X == 1) {
-                  mma_commit(&bar[B_KFREE0 + ((tt + 1) % C::NS)]);
-                  if (j + 1 == n - 1) mma_commit(&bar[B_QFREE]);
+                  commit(B_KFREE0 + ((tt + 1) % C::NS));
+                  if (j + 1 == n - 1) commit(B_QFREE);
                 }
               }
             }
@@ -304,14 +322,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         } else {
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
           issue_s(0, 0, t);
-          mma_commit(&bar[B_KFREE0 + (t % C::NS)]);
+          commit(B_KFREE0 + (t % C::NS));
           if (n > 1) {
             mbar_wait(&bar[B_KFULL0 + ((t + 1) % C::NS)], ((t + 1) / C::NS) & 1);
             tc_fence_after();
             issue_s(0, 1, t + 1);
-            mma_commit(&bar[B_KFREE0 + ((t + 1) % C::NS)]);
+            commit(B_KFREE0 + ((t + 1) % C::NS));
           }
-          if (n <= 2) mma_commit(&bar[B_QFREE]);
+          if (n <= 2) commit(B_QFREE);
           for (int j = 0; j < n; ++j) {
             const uint32_t tt = t + j;
             const int b = j & 1;
@@ -320,14 +338,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             if (j == 0) mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
             tc_fence_after();
             issue_pv(0, b, tt, j == 0);
-            mma_commit(&bar[B_VFREE0 + (tt % C::NS)]);
-            if (j == n - 1) mma_commit(&bar[B_OFULL0]);
+            commit(B_VFREE0 + (tt % C::NS));
+            if (j == n - 1) commit(B_OFULL0);
             if (j + 2 < n) {
               mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NS)], ((tt + 2) / C::NS) & 1);
               tc_fence_after();
               issue_s(0, b, tt + 2);
-              mma_commit(&bar[B_KFREE0 + ((tt + 2) % C::NS)]);
-              if (j + 2 == n - 1) mma_commit(&bar[B_QFREE]);
+              commit(B_KFREE0 + ((tt + 2) % C::NS));
+              if (j + 2 == n - 1) commit(B_QFREE);
             }
           }
           cnt[0] += (n + 1) >> 1;

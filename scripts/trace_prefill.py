@@ -10,7 +10,7 @@ t = W.make_tensors(b, device="cuda")
 pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq // b.hkv, b.d, torch.bfloat16, "cuda")
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
-tr = torch.zeros(64 * 16 + 64 * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(64 * 24 + 64 * 8, dtype=torch.int64, device="cuda")
 L = pk.lib()
 L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
 L.packinfer_debug_trace(tr.data_ptr())
@@ -18,8 +18,8 @@ pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 torch.cuda.synchronize()
 L.packinfer_debug_trace(None)
 A = tr.cpu().numpy().astype(np.int64)
-a = A[:1024].reshape(64, 16)
-U = A[1024:].reshape(64, 8)
+a = A[:64 * 24].reshape(64, 24)
+U = A[64 * 24:].reshape(64, 8)
 t0 = a[a > 0].min()
 names = ["mA_wait", "mA_got", "mA_iss", "mB_wait", "mB_got", "mB_iss",
          "sA_wS", "sA_gotS", "sA_p1", "sA_arrP", "sB_wS", "sB_gotS", "sB_p1", "sB_arrP"]
@@ -32,7 +32,8 @@ d = lambda x, y: a[:40, y] - a[:40, x]
 print("median sA: waitS", np.median(d(6, 7)), "pass1", np.median(d(7, 8)), "pass2+", np.median(d(8, 9)))
 print("median sB: waitS", np.median(d(10, 11)), "pass1", np.median(d(11, 12)), "pass2+", np.median(d(12, 13)))
 print("median mma: waitPA", np.median(d(0, 1)), "issueA", np.median(d(1, 2)), "waitPB", np.median(d(3, 4)), "issueB", np.median(d(4, 5)))
-print("median PV issue A", np.median(d(1, 14)), "S issue A", np.median(d(14, 2)), "PV issue B", np.median(d(4, 15)), "S issue B", np.median(d(15, 5)))
+print("median A: waitV", np.median(d(1, 16)), "PVissue", np.median(d(16, 14)), "waitK", np.median(d(14, 18)), "Sissue", np.median(d(18, 2)))
+print("median B: waitV", np.median(d(4, 17)), "PVissue", np.median(d(17, 15)), "waitK", np.median(d(15, 19)), "Sissue", np.median(d(19, 5)))
 print("tile period (A arrive->arrive)", np.median(np.diff(a[:40, 9])))
 
 u0 = U[U > 0].min()
