@@ -35,14 +35,19 @@ def needs_rebuild() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    lib = out or LIB
+    if not force and out is None and not needs_rebuild():
         return LIB
     nvcc = nvcc_path()
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC]
+    common += [f"-D{d}" for d in defines]
+    if defines:
+        objdir = os.path.join(PKG, "build", "_".join(defines))
+        os.makedirs(objdir, exist_ok=True)
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc, *ARCH, *common, "-c", os.path.join(CSRC, src), "-o", obj]
@@ -54,13 +59,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and (r.stdout or r.stderr):
             print(r.stdout, r.stderr, file=sys.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

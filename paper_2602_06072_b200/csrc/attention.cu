@@ -34,6 +34,10 @@
 #include "packinfer.h"
 #include "sm100.cuh"
 
+#ifndef PI_POLY_PAIRS
+#define PI_POLY_PAIRS 3   // of every 8 score pairs, this many take exp2 on the FMA pipe
+#endif
+
 namespace pi {
 
 using namespace sm100;
@@ -333,7 +337,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           for (int j = 0; j < n; ++j) {
             const uint32_t tt = t + j;
             const int b = j & 1;
+            trace_ev(p, tt, 0);
             mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
+            trace_ev(p, tt, 1);
             mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
             if (j == 0) mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
             tc_fence_after();
@@ -462,8 +468,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           mbar_wait(&bar[B_SFULL0 + b], (cnt[b] + kb) & 1);
           tc_fence_after();
           if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
-          // visible key columns of this row in this tile: [c_lo, c_hi)
-          int c_lo = 0, c_hi = 0;
+          // visible key columns of this row in this tile: [c_lo, c_hi).  Rows past row_count take
+          // the full-tile path (their results are discarded) so a warp never diverges on them.
+          int c_lo = 0, c_hi = 128;
           if (valid) {
             int lo_k = k0, hi_k = min(k0 + 128, se);
             if (last) {
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                   const uint64_t x =
                       f2_fma(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), SL2, NM);
                   uint64_t e;
-                  if (decltype(use_poly)::value && (i & 7) >= 5)
+                  if (decltype(use_poly)::value && (i & 7) >= 8 - PI_POLY_PAIRS)
                     e = ex2_poly2(x);
                   else
                     e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));

@@ -19,7 +19,8 @@ from typing import Optional
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpackinfer.so")
+_LIB_PATH = os.environ.get("PACKINFER_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                             "libpackinfer.so")
 
 PI_OK, PI_EINVAL, PI_ENOSPC, PI_ECUDA, PI_EUNSUP = 0, -1, -2, -3, -4
 PI_BF16, PI_FP32, PI_BF16_OUT_F32 = 0, 1, 2

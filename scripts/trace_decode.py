@@ -1,0 +1,33 @@
+"""CTA-0 timeline of the packed attention kernel on the cfg3 decode batch (debug hook)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from synth import workloads as W
+from paper_2602_06072_b200 import packinfer as pk
+
+b = W.cfg3_decode(1)
+t = W.make_tensors(b, device="cuda")
+pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq // b.hkv, b.d, torch.bfloat16, "cuda")
+out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
+pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
+tr = torch.zeros(64 * 24 + 64 * 8, dtype=torch.int64, device="cuda")
+L = pk.lib()
+L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
+L.packinfer_debug_trace(tr.data_ptr())
+pk.packinfer_attention_decode(pb.dp, t["q"], pb.k_buf, pb.v_buf, out, None, pb.partial_o, pb.partial_lse, 4)
+torch.cuda.synchronize()
+L.packinfer_debug_trace(None)
+A = tr.cpu().numpy().astype(np.int64)
+a = A[:64 * 24].reshape(64, 24)
+U = A[64 * 24:].reshape(64, 8)
+u0 = U[U > 0].min()
+w = pb.plan.decode_work
+print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done   (n_ktiles rows)")
+for i in range(30):
+    r = U[i]
+    item = (i * 148) // 8
+    print(f"{i:4d} " + " ".join(f"{(v - u0 if v else -1):9d}" for v in r[:7]),
+          int(w[item]["n_ktiles"]) if item < len(w) else -1, int(w[item]["row_count"]) if item < len(w) else -1)
+t0 = a[a > 0].min() if (a > 0).any() else 0
+print("softmax A per tile (gotS -> arriveP):", [int(x) for x in (a[:30, 9] - a[:30, 7])])
+print("softmax A wait S:", [int(x) for x in (a[:30, 7] - a[:30, 6])])

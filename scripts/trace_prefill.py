@@ -34,6 +34,7 @@ print("median sB: waitS", np.median(d(10, 11)), "pass1", np.median(d(11, 12)), "
 print("median mma: waitPA", np.median(d(0, 1)), "issueA", np.median(d(1, 2)), "waitPB", np.median(d(3, 4)), "issueB", np.median(d(4, 5)))
 print("median A: waitV", np.median(d(1, 16)), "PVissue", np.median(d(16, 14)), "waitK", np.median(d(14, 18)), "Sissue", np.median(d(18, 2)))
 print("median B: waitV", np.median(d(4, 17)), "PVissue", np.median(d(17, 15)), "waitK", np.median(d(15, 19)), "Sissue", np.median(d(19, 5)))
+print("softmax A phases: gotS->ld0", np.median(d(7, 20)), "h0 compute", np.median(d(20, 21)), "->ld1", np.median(d(21, 22)), "h1 compute", np.median(d(22, 23)), "->end", np.median(d(23, 8)))
 print("tile period (A arrive->arrive)", np.median(np.diff(a[:40, 9])))
 
 u0 = U[U > 0].min()
