@@ -96,7 +96,7 @@ struct AttnCfg {
   static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;   // + barriers + alignment slack
   static constexpr uint32_t FMT = F32 ? 2u : 1u;
-  static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 128, 0, 0);
+  static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 64, 0, 0);   // S in two N=64 halves
   // bf16: V is the MN-major B operand straight from TMA.  fp32 (kind::tf32): MN-major tf32 needs
   // the 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
   // P is stored as fp16 (10-bit mantissa: 8x smaller rounding than bf16; P <= 2^8 by the lazy
@@ -113,9 +113,13 @@ struct AttnCfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
+// S/P regions b = 0/1 complete per half-tile: SF[b][h] (S columns 64h..64h+63 landed), PHALF[b]
+// (P for keys 0..63 written), PFULL[b] (P for keys 64..127 written).  PVH[X]: the first half of
+// P.V into O slot X landed (only waited on for a rare mid-tile rescale).
 enum BarId {
   B_QFULL = 0, B_QFREE, B_KFULL0, B_KFULL1, B_KFREE0, B_KFREE1, B_VFULL0, B_VFULL1, B_VFREE0, B_VFREE1,
-  B_SFULL0, B_SFULL1, B_PFULL0, B_PFULL1, B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_COUNT
+  B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
+  B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_COUNT
 };
 
 // Makes the compiler treat r[] as produced after the preceding tcgen05.wait::ld.
@@ -131,6 +135,11 @@ struct Unit {
   int head0;   // Q head of tile A (tile B = head0 + 1); decode rows add their h_sub
   bool has_b;
 };
+
+// Static LPT schedule: units are sorted by cost (descending); round k hands CTA b the unit
+// k*G + b on even rounds and k*G + (G-1-b) on odd rounds ("snake"), which keeps per-CTA totals
+// within ~1% on the BASELINE.json batches without any inter-CTA communication.
+__device__ __forceinline__ int snake_unit(int k, int b, int G) { return k * G + ((k & 1) ? (G - 1 - b) : b); }
 
 __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
   Unit u;
@@ -172,8 +181,11 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       mbar_init(&bar[B_KFREE0 + s], 1);
       mbar_init(&bar[B_VFULL0 + s], F32 ? 32 : 1);
       mbar_init(&bar[B_VFREE0 + s], 1);
-      mbar_init(&bar[B_SFULL0 + s], 1);
+      mbar_init(&bar[B_SF00 + 2 * s], 1);
+      mbar_init(&bar[B_SF00 + 2 * s + 1], 1);
+      mbar_init(&bar[B_PHALF0 + s], 128);
       mbar_init(&bar[B_PFULL0 + s], 128);
+      mbar_init(&bar[B_PVH0 + s], 1);
       mbar_init(&bar[B_OFULL0 + s], 1);
       mbar_init(&bar[B_OFREE0 + s], 128);
     }
@@ -195,7 +207,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // ------------------------------------------------------------------ TMA producer
     // The whole warp walks the schedule (uniform values); one elected lane issues each copy.
     uint32_t t = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
       const Unit u = get_unit(p, w);
       for (int s = 0; s < u.wk.span_count; ++s) {
         const pi_span sp = p.spans[u.wk.span_begin + s];
@@ -240,18 +252,22 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       const uint64_t dv = F32 ? sdesc_sw128(sbase + C::OFF_V, 16, 1024)
                               : sdesc_sw128(sbase + C::OFF_V, C::ATOM_BYTES, 1024);
       constexpr uint64_t TILE16 = C::TILE_BYTES >> 4;
-      // S(X) = Q_X K(tt)^T into S/P region b
+      // S(X) = Q_X K(tt)^T into S/P region b, as two N = 64 halves (keys 0..63 / 64..127) so the
+      // softmax can start on the first half while the second is computed.
       auto issue_s = [&](int X, int b, uint32_t tt) {
         const uint64_t aq = dq + X * TILE16;
         const uint64_t bk = dk + (tt % C::NS) * TILE16;
         const uint32_t d_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < C::QK_STEPS; ++kk) {
-            const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
-            mma_ss<F32>(d_tmem, aq + off, bk + off, C::IDESC_QK, kk > 0 ? 1u : 0u);
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int kk = 0; kk < C::QK_STEPS; ++kk) {
+              const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
+              mma_ss<F32>(d_tmem + h * 64, aq + off, bk + off + h * (8192 >> 4), C::IDESC_QK, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&bar[B_SF00 + 2 * b + h]);
           }
-          mma_commit(&bar[B_SFULL0 + b]);
         }
         __syncwarp();
       };
@@ -259,14 +275,15 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         if (elect_one()) mma_commit(&bar[id]);
         __syncwarp();
       };
-      // O_X += P(region b) V(tt)
-      auto issue_pv = [&](int X, int b, uint32_t tt, bool first) {
+      // O_X += P(region b) V(tt) for keys [64h, 64h + 64)
+      auto issue_pv = [&](int X, int b, uint32_t tt, bool first, int h) {
         const uint64_t bv = dv + (tt % C::NS) * TILE16;
         const uint32_t p_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
         const uint32_t d_tmem = tmem + (X ? C::TM_O1 : C::TM_O0);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < C::PV_STEPS; ++kk) {
+          for (int q = 0; q < C::PV_STEPS / 2; ++q) {
+            const int kk = h * (C::PV_STEPS / 2) + q;
             const uint64_t off = F32 ? (uint64_t)(((kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32) >> 4)
                                      : (uint64_t)((kk * C::KEYS_PER_PV_STEP * 128) >> 4);
             mma_ts<F32>(d_tmem, p_tmem + kk * 8, bv + off, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
@@ -274,7 +291,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         }
         __syncwarp();
       };
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
         const Unit u = get_unit(p, w);
         const int n = u.wk.n_ktiles;
         trace_unit(p, item, 0);
@@ -284,7 +301,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         trace_unit(p, item, 2);
         tc_fence_after();
         if (u.has_b) {
-          // ---- pair unit: slot X keeps its S/P region X; ping-pong between the two tiles
+          // ---- pair unit: slot X keeps S/P region X; ping-pong between the two tiles
           issue_s(0, 0, t);
           issue_s(1, 1, t);
           commit(B_KFREE0 + (t % C::NS));
@@ -293,13 +310,16 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             const uint32_t tt = t + j;
             for (int X = 0; X < 2; ++X) {
               trace_ev(p, tt, 0 + 3 * X);
-              mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
+              mbar_wait(&bar[B_PHALF0 + X], (cnt[X] + j) & 1);
               trace_ev(p, tt, 1 + 3 * X);
               if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
               if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
-              trace_ev(p, tt, 16 + X);
               tc_fence_after();
-              issue_pv(X, X, tt, j == 0);
+              issue_pv(X, X, tt, j == 0, 0);
+              commit(B_PVH0 + X);
+              mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
+              tc_fence_after();
+              issue_pv(X, X, tt, false, 1);
               trace_ev(p, tt, 14 + X);
               if (X == 1) commit(B_VFREE0 + (tt % C::NS));
               if (j == n - 1) {
@@ -309,7 +329,6 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                   mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NS)], ((tt + 1) / C::NS) & 1);
                   tc_fence_after();
                 }
-                trace_ev(p, tt, 18 + X);
                 issue_s(X, X, tt + 1);
                 trace_ev(p, tt, 2 + 3 * X);
                 if (X == 1) {
@@ -338,12 +357,16 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             const uint32_t tt = t + j;
             const int b = j & 1;
             trace_ev(p, tt, 0);
-            mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
+            mbar_wait(&bar[B_PHALF0 + b], (cnt[b] + (j >> 1)) & 1);
             trace_ev(p, tt, 1);
             mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
             if (j == 0) mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
             tc_fence_after();
-            issue_pv(0, b, tt, j == 0);
+            issue_pv(0, b, tt, j == 0, 0);
+            commit(B_PVH0);
+            mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
+            tc_fence_after();
+            issue_pv(0, b, tt, false, 1);
             commit(B_VFREE0 + (tt % C::NS));
             if (j == n - 1) commit(B_OFULL0);
             if (j + 2 < n) {
@@ -369,7 +392,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // Q rows are addressed through the plan's row table: lane g gathers rows 4g..4g+3 of each tile
     // (one gather4 per 128-byte atom column) straight into the SWIZZLE_128B K-major operand layout.
     uint32_t item = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
       const Unit u = get_unit(p, w);
       const int nt = u.has_b ? 2 : 1;
       trace_unit(p, item, 4);
@@ -401,7 +424,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // ------------------------------------------------------------------ fp32 only: V^T staging
     if constexpr (F32) {
       uint32_t t = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
         const Unit u = get_unit(p, w);
         const float* vsrc = reinterpret_cast<const float*>(p.v_buf) + (int64_t)u.kvh * p.buffer_tokens * D;
         for (int s = 0; s < u.wk.span_count; ++s) {
@@ -438,9 +461,23 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t o_tm = tmem + lane_base + (X ? C::TM_O1 : C::TM_O0);
     uint32_t cnt[2] = {0, 0}, ix = 0, t = 0;
+    uint32_t pvh = 0;                       // completions so far of PVH[X] (this slot's P.V halves)
     const float NEG_INF = -INFINITY;
     const float sl2 = p.scale_log2;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    // O_X *= alpha, all columns (lazy rescale; rare)
+    auto rescale_o = [&](float alpha) {
+#pragma unroll
+      for (int c4 = 0; c4 < D / 32; ++c4) {
+        uint32_t o32[32];
+        tmem_ld32(o_tm + c4 * 32, o32);
+        tmem_wait_ld();
+        reg_fence(o32);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o32[i] = __float_as_uint(__uint_as_float(o32[i]) * alpha);
+        tmem_st32(o_tm + c4 * 32, o32);
+      }
+    };
+    for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
       const Unit u = get_unit(p, w);
       const pi_work& wk = u.wk;
       const int n = wk.n_ktiles;
@@ -464,10 +501,6 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           const int b = u.has_b ? X : (int)(j & 1);          // S/P region of this tile
           const uint32_t kb = u.has_b ? j : (j >> 1);        // use index of region b in this unit
           const uint32_t s_tm = tmem + lane_base + (b ? C::TM_S1 : C::TM_S0);
-          if (row_id == 0) trace_ev(p, t + j, 6 + 4 * X);
-          mbar_wait(&bar[B_SFULL0 + b], (cnt[b] + kb) & 1);
-          tc_fence_after();
-          if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
           // visible key columns of this row in this tile: [c_lo, c_hi).  Rows past row_count take
           // the full-tile path (their results are discarded) so a warp never diverges on them.
           int c_lo = 0, c_hi = 128;
@@ -480,16 +513,20 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             c_lo = lo_k - k0;
             c_hi = hi_k - k0;
           }
-          if (warp_any) {
-            const bool full = (c_lo == 0 && c_hi == 128);
-            // Streaming single pass over two 64-column halves: each S element is read from TMEM
-            // once.  The running max is updated per half (lazily: only when it grows by > 2^8);
-            // if the second half raises it, the first half's P (already in TMEM) and O are rescaled.
-            float ps[4] = {0.f, 0.f, 0.f, 0.f};
-            float alpha_o = 1.0f;     // pending O rescale for this tile
-            bool any_o = false;
+          const bool full = (c_lo == 0 && c_hi == 128);
+          float ps[4] = {0.f, 0.f, 0.f, 0.f};
+          // Streaming single pass over two 64-column halves, each released to the tensor core as
+          // soon as it is written: each S element is read from TMEM once; the running max is lazy
+          // (updated only when it grows by > 2^8).  A jump in the first half rescales O before any
+          // P of this tile is used; a jump in the second half rescales O after the first half's
+          // P.V has landed (O then holds it, so one rescale covers both).
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < 2; ++h) {
+            if (row_id == 0 && h == 0) trace_ev(p, t + j, 6 + 4 * X);
+            mbar_wait(&bar[B_SF00 + 2 * b + h], (cnt[b] + kb) & 1);
+            tc_fence_after();
+            if (row_id == 0 && h == 0) trace_ev(p, t + j, 7 + 4 * X);
+            if (warp_any) {
               uint32_t r[64];
               tmem_ld32(s_tm + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
               tmem_ld32(s_tm + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
@@ -510,39 +547,37 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
               if (__any_sync(0xffffffffu, need)) {
                 const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
-                if (h == 1) {
-                  // P of the first half was exponentiated against the old max
-#pragma unroll
-                  for (int c = 0; c < (F32 ? 64 : 32); c += 32) {
-                    uint32_t q32[32];
-                    tmem_ld32(s_tm + c, q32);
-                    tmem_wait_ld();
-                    reg_fence(q32);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                      q32[i] = F32 ? __float_as_uint(__uint_as_float(q32[i]) * alpha)
-                                   : pack_f16(__half2float(__ushort_as_half((unsigned short)(q32[i] & 0xffffu))) * alpha,
-                                              __half2float(__ushort_as_half((unsigned short)(q32[i] >> 16))) * alpha);
-                    tmem_st32(s_tm + c, q32);
+                if (h == 0) {
+                  if (j > 0) {
+                    // pair units: P.V(j-1) completed before S(j) did (in-order tcgen05 pipe);
+                    // single-tile units issue P.V(j-1) after S(j): wait for it
+                    if (!u.has_b) {
+                      const uint32_t tp = t + j - 1;
+                      mbar_wait(&bar[B_VFREE0 + (tp % C::NS)], (tp / C::NS) & 1);
+                      tc_fence_after();
+                    }
+                    rescale_o(alpha);
                   }
+                } else {
+                  // the first half's P.V (issued with the old max) must have landed in O
+                  mbar_wait(&bar[B_PVH0 + X], (pvh + j) & 1);
+                  tc_fence_after();
+                  rescale_o(alpha);
 #pragma unroll
-                  for (int k = 0; k < 4; ++k) ps[k] *= alpha;
+                  for (int q = 0; q < 4; ++q) ps[q] *= alpha;
                 }
-                alpha_o *= alpha;
-                any_o = true;
                 if (need) {
                   l *= alpha;
                   m_ref = m_new;
                 }
               }
               if (m_ref == NEG_INF) m_ref = m_new;
-              // P = exp2(s * scale_log2 - m_ref): FFMA2 for the argument, 3 of 8 pairs on the FMA
-              // pipe (ex2_poly2), the rest on MUFU; masked columns hold -inf -> 0
+              // P = exp2(s * scale_log2 - m_ref): FFMA2 for the argument, PI_POLY_PAIRS of 8 pairs on
+              // the FMA pipe (ex2_poly2), the rest on MUFU; masked columns hold -inf -> 0
               const bool live = m_ref != NEG_INF;
               const float nm = live ? -m_ref : NEG_INF;
               const uint64_t SL2 = f2(sl2, sl2), NM = f2(nm, nm);
               uint64_t acc0 = f2(ps[0], ps[1]), acc1 = f2(ps[2], ps[3]);
-              // two branch-free bodies: full tiles offload 3 of 8 pairs to the FMA pipe
               auto body = [&](auto use_poly) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
@@ -576,36 +611,13 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                 tmem_st32(s_tm + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
                 tmem_st32(s_tm + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
               }
+              tmem_wait_st();
             }
-            if (row_id == 0) trace_ev(p, t + j, 8 + 4 * X);
-            const bool any_need = any_o && j > 0;   // tile 0 overwrites O (accumulate = 0)
-            const float alpha = alpha_o;
-            if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
-            // ---- lazy O rescale (rare): before P(j) is released to the tensor core
-            if (any_need) {
-              if (!u.has_b && j > 0) {
-                // single-tile unit: P.V(j-1) may still be in flight; wait until it has landed
-                const uint32_t tp = t + j - 1;
-                mbar_wait(&bar[B_VFREE0 + (tp % C::NS)], (tp / C::NS) & 1);
-                tc_fence_after();
-              }
-              // (pair units: every earlier P.V of this slot completed before S(j) did)
-#pragma unroll
-              for (int c4 = 0; c4 < D / 32; ++c4) {
-                uint32_t o32[32];
-                tmem_ld32(o_tm + c4 * 32, o32);
-                tmem_wait_ld();
-                reg_fence(o32);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) o32[i] = __float_as_uint(__uint_as_float(o32[i]) * alpha);
-                tmem_st32(o_tm + c4 * 32, o32);
-              }
-            }
-            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bar[(h == 0 ? B_PHALF0 : B_PFULL0) + b]);
+            if (row_id == 0 && h == 1) trace_ev(p, t + j, 9 + 4 * X);
           }
-          tc_fence_before();
-          mbar_arrive(&bar[B_PFULL0 + b]);
-          if (row_id == 0) trace_ev(p, t + j, 9 + 4 * X);
+          if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
         }
       }
       // ---------------- epilogue: O / l -> out (or partial), lse
@@ -670,6 +682,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         cnt[0] += (n + 1) >> 1;
         cnt[1] += n >> 1;
       }
+      pvh += n;
       t += n;
       ++ix;
     }
