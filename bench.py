@@ -308,9 +308,8 @@ def main():
 
     b = make_workload("cfg2", 0 if args.shard == "heads" else rank)
     if args.shard == "heads" and world > 1:
-        assert b.hkv % world == 0
-        hc = b.hkv // world
-        h0 = rank * hc
+        from paper_2602_06072_b200 import shard
+        h0, hc = shard.kv_head_shard(b.hkv, rank, world)
     else:
         h0, hc = 0, b.hkv
     runner = Runner(b, dev, h0, hc, seed=b.seed)

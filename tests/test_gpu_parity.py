@@ -161,14 +161,23 @@ def _sampled_rows(b, rng, per_req=3):
     return rows
 
 
-@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4_decode", "cfg4_prefill"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4_decode", "cfg4_prefill", "cfg5"])
 def test_full_size_sampled(name):
-    """BASELINE.json full sizes in bench.py's launch configuration; oracle on sampled rows."""
+    """BASELINE.json full sizes in bench.py's launch configuration; oracle on sampled rows.
+    cfg5 (Llama-3-70B shape) splits each 131,072-token request into 16 pieces across groups
+    (prefill rows attend to earlier pieces in other groups' buffers; decode rows merge partials)."""
     b = W.make_batch(name)
     t = W.make_tensors(b, device="cuda")
     out, lse, pb = H.run_batch(b, t, C=8192, delta=32 if "cfg4" in name else 0, out_f32=True)
     rng = np.random.default_rng(0)
-    rows = _sampled_rows(b, rng)
+    rows = _sampled_rows(b, rng, per_req=1 if name == "cfg5" else 3)
+    if name == "cfg5":
+        # every piece boundary of the 128k requests (first / last row of each 8192-token piece)
+        for i in range(b.n):
+            if int(b.q_len[i]) > 8192:
+                rows += [(i, a) for a in range(0, int(b.q_len[i]), 8192)]
+                rows += [(i, a + 8191) for a in range(0, int(b.q_len[i]), 8192)]
+        rows = sorted(set(rows))
     ro, rl = OA.attention_rows(t["q"].cpu(), t["k_paged"].cpu(), t["v_paged"].cpu(), t["block_table"].cpu(),
                                b.kv_len, b.q_len, b.page_size, rows)
     q_off = np.concatenate([[0], np.cumsum(b.q_len)])
