@@ -362,7 +362,10 @@ def main():
         dms = timed_steps(rd, max(3, args.steps), args.warmup, dist_on) / max(3, args.steps)
         _, dec_ms = rd.kernel_ms()
         ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
-        result["decode"] = {"workload": bd.name + " (BASELINE.json configs[2])", "ms_per_step": dms,
+        dtraffic = None
+        if os.path.exists(tf):
+            dtraffic = json.load(open(tf)).get("decode_attention_dram_bytes")
+        result["decode"] = {"workload": bd.name + " (BASELINE.json configs[2])", "ms_per_step": dms, "traffic": dtraffic,
                             "kernel_ms": dec_ms, "kv_bytes": kvb, "achieved_gbs": ach, "peak_gbs": peaks["hbm_gbs"],
                             "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
                             "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9,
