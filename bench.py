@@ -322,12 +322,15 @@ def main():
     clocks = sampler.stop()
     ms_step = total_ms / args.steps
     pre_ms, _ = runner.kernel_ms()
+    units_total = flops
     if dist_on:
         import torch.distributed as dist
         tt = torch.tensor([ms_step, pre_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)           # step time = slowest rank
         ms_step, pre_ms = float(tt[0]), float(tt[1])
-    units_total = flops * (world if args.shard == "group" else 1)
+        ft = torch.tensor([float(flops)], device=dev, dtype=torch.float64)
+        dist.all_reduce(ft, op=dist.ReduceOp.SUM)           # work of every rank's shard / batch
+        units_total = float(ft[0])
     value = units_total / (ms_step * 1e-3) / 1e12
     pc = runner.pbs[0].plan.c
     achieved = flops / (pre_ms * 1e-3) / 1e12
@@ -376,6 +379,11 @@ def main():
 
     if not args.no_e2e:
         e_ms, h2d, d2h = e2e_steps(b, runner, max(2, min(args.steps, 5)))
+        if dist_on:
+            import torch.distributed as dist
+            et = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e_ms = float(et[0])
         result["e2e"] = {"value": units_total / (e_ms * 1e-3) / 1e12,
                          "unit": "TFLOP/s", "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
