@@ -60,7 +60,8 @@ typedef enum {
   PI_EINVAL = -1, /* invalid argument (see packinfer_last_error)                         */
   PI_ENOSPC = -2, /* caller buffer too small; required sizes were written back          */
   PI_ECUDA = -3,  /* a CUDA runtime/driver call failed (launch or tensor-map encode)     */
-  PI_EUNSUP = -4  /* unsupported dtype / head_dim / device (needs sm_100a)              */
+  PI_EUNSUP = -4, /* unsupported dtype / head_dim / device (needs sm_100a)              */
+  PI_EREGROUP = -5 /* decode headroom exhausted: regroup (re-plan + relayout)      */
 } pi_status;
 
 typedef enum {
@@ -150,6 +151,10 @@ typedef struct {
   int64_t valid_cells, tile_cells;         /* prefill tile efficiency (reading R-eta)     */
   int32_t discrepancy;                     /* Eq. 3                               */
   int32_t reserved;
+  int32_t* append_pos;   /* [n] buffer token where request i's next decode token goes (headroom,
+                            P:306-309), -1 if none (not a decode request / headroom exhausted) */
+  int64_t drift;         /* Eq. 4 dL = max_g L(S_g) - min_g L(S_g) including appended tokens    */
+  int64_t appended_total;
   void* arena;  size_t arena_bytes;        /* the host arena holding every table          */
 } pi_plan;
 
@@ -166,6 +171,21 @@ PI_API pi_status packinfer_plan(int32_t n, const int32_t* kv_len, const int32_t*
                          const pi_config* cfg, void* host_arena, size_t arena_bytes,
                          pi_plan* out);
 
+/* Decode loop without re-consolidation.  Same inputs as packinfer_plan
+ * (the lengths of the last consolidation) plus appended[n] (host): the number of decode tokens
+ * request i has appended into its suffix headroom since then (packinfer_append_kv).  Groups,
+ * offsets and the copy plan are those of packinfer_plan on the same inputs (bit-identical); the
+ * execution domain covers kv_len[i] + appended[i] keys.  appended[i] > 0 requires q_len[i] == 1;
+ * appended[i] > headroom returns PI_EREGROUP (the caller must regroup: re-plan + relayout).  */
+PI_API pi_status packinfer_plan_step(int32_t n, const int32_t* kv_len, const int32_t* q_len,
+                                     const int32_t* prefix_id, int32_t n_prefix,
+                                     const int32_t* prefix_len, const int32_t* appended,
+                                     const pi_config* cfg, void* host_arena, size_t arena_bytes,
+                                     pi_plan* out);
+
+/* Eq. 4: 1 iff steps * drift >= capacity / 2 (inclusive, exact integer test). */
+PI_API int32_t packinfer_should_regroup(int32_t steps, int64_t drift, int32_t capacity);
+
 /* Device view of a plan: the same tables in device memory. */
 typedef struct {
   const pi_copy* copies;  const int64_t* copy_prefix; int32_t n_copies; int64_t copy_tokens;
@@ -175,6 +195,7 @@ typedef struct {
   const pi_merge* merges; int32_t n_merges; int32_t n_partial_slots;
   int64_t buffer_tokens;
   int32_t n_requests, total_q, gqa_ratio, tile_k;
+  const int32_t* append_pos;                 /* [n_requests] (see pi_plan)                      */
 } pi_device_plan;
 
 /* Enqueue one host->device copy of plan->arena into dev_arena (device, >= plan->arena_bytes,
@@ -192,6 +213,15 @@ PI_API pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void* k_p
                                 int32_t max_blocks, int32_t page_size, int32_t hkv_total,
                                 int32_t hkv_begin, int32_t hkv_count, int32_t head_dim,
                                 pi_dtype dt, void* k_buf, void* v_buf, pi_stream_t stream);
+
+/* Append one decode token per request into its headroom slot (plan->append_pos):
+ * k_new / v_new [n_requests, hkv_total, head_dim] (host layout of one paged token row; rows of
+ * requests without a slot are ignored), heads [hkv_begin, hkv_begin + hkv_count) -> k_buf / v_buf
+ * (V stored as in packinfer_relayout_kv).  Follow with packinfer_plan_step(appended + 1).      */
+PI_API pi_status packinfer_append_kv(const pi_device_plan* dp, const void* k_new, const void* v_new,
+                                     int32_t hkv_total, int32_t hkv_begin, int32_t hkv_count,
+                                     int32_t head_dim, pi_dtype dt, void* k_buf, void* v_buf,
+                                     pi_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
  * Packed attention ("union of valid query-key regions"; P:172 one launch for every

@@ -32,6 +32,7 @@ const char* packinfer_strerror(pi_status s) {
     case PI_ENOSPC: return "buffer too small";
     case PI_ECUDA: return "CUDA error";
     case PI_EUNSUP: return "unsupported";
+    case PI_EREGROUP: return "headroom exhausted: regroup";
   }
   return "unknown status";
 }
@@ -57,10 +58,25 @@ pi_status packinfer_plan(int32_t n, const int32_t* kv_len, const int32_t* q_len,
                          const int32_t* prefix_id, int32_t n_prefix, const int32_t* prefix_len,
                          const pi_config* cfg, void* host_arena, size_t arena_bytes,
                          pi_plan* out) {
-  pi_status s = pi::plan_impl(n, kv_len, q_len, prefix_id, n_prefix, prefix_len, cfg,
+  pi_status s = pi::plan_impl(n, kv_len, q_len, prefix_id, n_prefix, prefix_len, nullptr, cfg,
                               host_arena, arena_bytes, out);
   if (s == PI_OK) pi::ok();
   return s;
+}
+
+pi_status packinfer_plan_step(int32_t n, const int32_t* kv_len, const int32_t* q_len,
+                              const int32_t* prefix_id, int32_t n_prefix, const int32_t* prefix_len,
+                              const int32_t* appended, const pi_config* cfg, void* host_arena,
+                              size_t arena_bytes, pi_plan* out) {
+  pi_status s = pi::plan_impl(n, kv_len, q_len, prefix_id, n_prefix, prefix_len, appended, cfg,
+                              host_arena, arena_bytes, out);
+  if (s == PI_OK) pi::ok();
+  return s;
+}
+
+int32_t packinfer_should_regroup(int32_t steps, int64_t drift, int32_t capacity) {
+  // Eq. 4: t * dL >= C / 2, exact in integers (2 t dL >= C)
+  return (2 * (int64_t)steps * drift >= (int64_t)capacity) ? 1 : 0;
 }
 
 pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, size_t dev_bytes,
@@ -93,6 +109,7 @@ pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, size_t dev_by
   out->merges = static_cast<const pi_merge*>(dev(p->merges));
   out->n_merges = p->n_merges;
   out->n_partial_slots = p->n_partial_slots;
+  out->append_pos = static_cast<const int32_t*>(dev(p->append_pos));
   out->buffer_tokens = p->buffer_tokens;
   out->n_requests = p->n_requests;
   out->total_q = p->total_q;

@@ -14,6 +14,7 @@ pi_status ok();
 
 pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
                     const int32_t* prefix_id, int32_t n_prefix, const int32_t* prefix_len,
-                    const pi_config* cfg, void* arena, size_t arena_bytes, pi_plan* out);
+                    const int32_t* appended, const pi_config* cfg, void* arena, size_t arena_bytes,
+                    pi_plan* out);
 
 }  // namespace pi

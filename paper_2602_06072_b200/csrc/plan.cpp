@@ -52,7 +52,8 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
                     const int32_t* prefix_id, int32_t n_prefix, const int32_t* prefix_len,
-                    const pi_config* cfg, void* arena, size_t arena_bytes, pi_plan* out) {
+                    const int32_t* appended, const pi_config* cfg, void* arena, size_t arena_bytes,
+                    pi_plan* out) {
   if (!cfg || !out) return fail(PI_EINVAL, "cfg and out must be non-NULL");
   if (n < 0 || n_prefix < 0) return fail(PI_EINVAL, "negative n / n_prefix");
   if (n > 0 && (!kv_len || !q_len)) return fail(PI_EINVAL, "kv_len/q_len NULL with n > 0");
@@ -83,6 +84,19 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
     total_q += q;
   }
   if (total_q > INT32_MAX) return fail(PI_EINVAL, "total_q exceeds int32");
+  // Decode-loop steps since the last consolidation: appended[i] new tokens of decode
+  // request i sit in its suffix headroom; the layout (Parts 1-2) is planned from kv_len, the
+  // execution domain from kv_len + appended.
+  int64_t total_appended = 0;
+  for (int32_t i = 0; appended && i < n; ++i) {
+    if (appended[i] < 0) return fail(PI_EINVAL, "appended[" + std::to_string(i) + "] < 0");
+    if (appended[i] > 0 && q_len[i] != 1)
+      return fail(PI_EINVAL, "appended tokens are only defined for decode requests (q_len == 1)");
+    if (appended[i] > delta)
+      return fail(PI_EREGROUP, "appended[" + std::to_string(i) + "] exceeds the headroom: re-plan (regroup)");
+    total_appended += appended[i];
+  }
+  auto app = [&](int32_t i) -> int64_t { return appended ? appended[i] : 0; };
 
   // ---------------- pieces (reading R5: split into C-token pieces, prefix dropped) ---------
   std::vector<Piece> pieces;
@@ -345,7 +359,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       }
       const Piece& pc = pieces[e.piece];
       if (q_len[pc.request] != 1) continue;
-      emit_decode(g, {pc.request}, piece_buf(e.piece), offsets[e.piece].l_suffix);
+      const bool last_piece = e.piece == first_piece[pc.request + 1] - 1;
+      emit_decode(g, {pc.request}, piece_buf(e.piece), offsets[e.piece].l_suffix + (last_piece ? app(pc.request) : 0));
     }
   }
   // partial slots for rows with more than one decode item (reading R10 / Q19)
@@ -372,6 +387,26 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   };
   lpt(pwork);
   lpt(dwork);
+
+  // ---------------- decode loop: next append slot per request, group drift (Eq. 4) ----------
+  std::vector<int32_t> append_pos(std::max(n, 1), -1);
+  std::vector<int64_t> gload(G, 0);
+  for (int32_t g = 0; g < G; ++g) gload[g] = groups[g].load;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t k = first_piece[i + 1] - 1;  // last piece holds the growing suffix
+    const Piece& pc = pieces[k];
+    if (q_len[i] == 1) {
+      gload[pc.group] += app(i);
+      if (app(i) < delta)
+        append_pos[i] = (int32_t)(groups[pc.group].base + offsets[k].d_suffix + offsets[k].l_suffix + app(i));
+    }
+  }
+  int64_t drift = 0;
+  if (G > 0) {
+    int64_t mx = gload[0], mn = gload[0];
+    for (int64_t x : gload) { mx = std::max(mx, x); mn = std::min(mn, x); }
+    drift = mx - mn;
+  }
 
   // ---------------- reported quantities ------------------------------------------------------
   int64_t sumL2 = 0;
@@ -404,6 +439,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const size_t o_rows = reserve(sizeof(pi_row) * rows.size());
   const size_t o_spans = reserve(sizeof(pi_span) * spans.size());
   const size_t o_merges = reserve(sizeof(pi_merge) * merges.size());
+  const size_t o_append = reserve(sizeof(int32_t) * std::max(n, 1));
   const size_t need = std::max<size_t>(off, 256);
 
   std::memset(out, 0, sizeof(*out));
@@ -428,6 +464,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   out->valid_cells = valid_cells;
   out->tile_cells = tile_cells;
   out->discrepancy = (int32_t)disc;
+  out->drift = drift;
+  out->appended_total = total_appended;
   out->arena_bytes = need;
   if (!arena || arena_bytes < need) {
     out->arena = nullptr;
@@ -446,6 +484,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   out->rows = reinterpret_cast<pi_row*>(A + o_rows);
   out->spans = reinterpret_cast<pi_span*>(A + o_spans);
   out->merges = reinterpret_cast<pi_merge*>(A + o_merges);
+  out->append_pos = reinterpret_cast<int32_t*>(A + o_append);
   for (int32_t k = 0; k < NP; ++k) {
     const Piece& pc = pieces[k];
     out->pieces[k] = {pc.request, pc.piece, pc.kv_begin, pc.kv_len, pc.group};
@@ -461,6 +500,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   if (!rows.empty()) std::memcpy(out->rows, rows.data(), sizeof(pi_row) * rows.size());
   if (!spans.empty()) std::memcpy(out->spans, spans.data(), sizeof(pi_span) * spans.size());
   if (!merges.empty()) std::memcpy(out->merges, merges.data(), sizeof(pi_merge) * merges.size());
+  std::memcpy(out->append_pos, append_pos.data(), sizeof(int32_t) * std::max(n, 1));
   return PI_OK;
 }
 

@@ -104,7 +104,60 @@ __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
   }
 }
 
+// One warp per request: copy its new token's hkv_count*d K and V elements into the headroom slot
+// append_pos[i] of every local head ("allows multiple decoding iterations to proceed
+// without triggering re-alignment").
+__global__ void __launch_bounds__(256) append_kernel(const int32_t* __restrict__ append_pos, int32_t n,
+                                                      const uint8_t* kn, const uint8_t* vn, int64_t token_bytes,
+                                                      int64_t head_off_bytes, int32_t chunks, int32_t head_chunks,
+                                                      int64_t buf_head_bytes, uint8_t* kb, uint8_t* vb,
+                                                      int32_t v_to_f16) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int32_t dst = append_pos[i];
+  if (dst < 0) return;
+  const int64_t row_bytes = (int64_t)head_chunks * 16;
+  const uint8_t* ks = kn + i * token_bytes + head_off_bytes;
+  const uint8_t* vs = vn + i * token_bytes + head_off_bytes;
+  for (int c = lane; c < chunks; c += 32) {
+    const int h = c / head_chunks, cc = c % head_chunks;
+    const int64_t d = h * buf_head_bytes + (int64_t)dst * row_bytes + (int64_t)cc * 16;
+    const uint4 kv = reinterpret_cast<const uint4*>(ks)[c];
+    const uint4 vv = reinterpret_cast<const uint4*>(vs)[c];
+    *reinterpret_cast<uint4*>(kb + d) = kv;
+    *reinterpret_cast<uint4*>(vb + d) = v_to_f16 ? bf16x8_to_f16x8(vv) : vv;
+  }
+}
+
 }  // namespace pi
+
+extern "C" pi_status packinfer_append_kv(const pi_device_plan* dp, const void* k_new, const void* v_new,
+                                         int32_t hkv_total, int32_t hkv_begin, int32_t hkv_count,
+                                         int32_t head_dim, pi_dtype dt, void* k_buf, void* v_buf,
+                                         pi_stream_t stream) {
+  using namespace pi;
+  if (!dp) return fail(PI_EINVAL, "device plan is NULL");
+  if (dp->n_requests == 0 || dp->buffer_tokens == 0) return ok();
+  if (!k_new || !v_new || !k_buf || !v_buf || !dp->append_pos) return fail(PI_EINVAL, "NULL pointer argument");
+  if (hkv_total < 1 || hkv_begin < 0 || hkv_count < 1 || hkv_begin + hkv_count > hkv_total)
+    return fail(PI_EINVAL, "KV head range out of bounds");
+  if (dt != PI_BF16 && dt != PI_FP32) return fail(PI_EUNSUP, "dtype must be PI_BF16 or PI_FP32");
+  const int es = dt == PI_BF16 ? 2 : 4;
+  if ((head_dim * es) % 16) return fail(PI_EINVAL, "head_dim * element size must be a multiple of 16 bytes");
+  if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new) |
+       reinterpret_cast<uintptr_t>(k_buf) | reinterpret_cast<uintptr_t>(v_buf)) % 16)
+    return fail(PI_EINVAL, "tensors must be 16-byte aligned");
+  const int32_t head_chunks = head_dim * es / 16;
+  const unsigned blocks = (unsigned)((dp->n_requests + 7) / 8);
+  append_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      dp->append_pos, dp->n_requests, static_cast<const uint8_t*>(k_new), static_cast<const uint8_t*>(v_new),
+      (int64_t)hkv_total * head_dim * es, (int64_t)hkv_begin * head_dim * es, hkv_count * head_chunks, head_chunks,
+      dp->buffer_tokens * head_dim * es, static_cast<uint8_t*>(k_buf), static_cast<uint8_t*>(v_buf),
+      dt == PI_BF16 ? 1 : 0);
+  pi_status s = cuda_check(cudaGetLastError(), "append_kernel launch");
+  return s == PI_OK ? ok() : s;
+}
 
 extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void* k_paged, const void* v_paged,
                                            const int32_t* block_table, int32_t max_blocks, int32_t page_size,

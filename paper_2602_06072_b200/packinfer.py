@@ -22,13 +22,14 @@ import numpy as np
 _LIB_PATH = os.environ.get("PACKINFER_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                              "libpackinfer.so")
 
-PI_OK, PI_EINVAL, PI_ENOSPC, PI_ECUDA, PI_EUNSUP = 0, -1, -2, -3, -4
+PI_OK, PI_EINVAL, PI_ENOSPC, PI_ECUDA, PI_EUNSUP, PI_EREGROUP = 0, -1, -2, -3, -4, -5
 PI_BF16, PI_FP32, PI_BF16_OUT_F32 = 0, 1, 2
 
 EXPORTS = [
     "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
     "packinfer_plan", "packinfer_plan_upload", "packinfer_relayout_kv",
     "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_merge",
+    "packinfer_plan_step", "packinfer_should_regroup", "packinfer_append_kv",
 ]
 
 
@@ -73,6 +74,7 @@ class pi_plan(C.Structure):
                 ("eta_num", C.c_int64), ("eta_den", C.c_int64),
                 ("valid_cells", C.c_int64), ("tile_cells", C.c_int64),
                 ("discrepancy", C.c_int32), ("reserved", C.c_int32),
+                ("append_pos", C.c_void_p), ("drift", C.c_int64), ("appended_total", C.c_int64),
                 ("arena", C.c_void_p), ("arena_bytes", C.c_size_t)]
 
 
@@ -85,7 +87,7 @@ class pi_device_plan(C.Structure):
                 ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
                 ("buffer_tokens", C.c_int64),
                 ("n_requests", C.c_int32), ("total_q", C.c_int32), ("gqa_ratio", C.c_int32),
-                ("tile_k", C.c_int32)]
+                ("tile_k", C.c_int32), ("append_pos", C.c_void_p)]
 
 
 _lib = None
@@ -107,6 +109,13 @@ def lib():
         L.packinfer_plan.restype = C.c_int
         L.packinfer_plan.argtypes = [i32, vp, vp, vp, i32, vp, C.POINTER(pi_config), vp, C.c_size_t,
                                      C.POINTER(pi_plan)]
+        L.packinfer_plan_step.restype = C.c_int
+        L.packinfer_plan_step.argtypes = [i32, vp, vp, vp, i32, vp, vp, C.POINTER(pi_config), vp, C.c_size_t,
+                                          C.POINTER(pi_plan)]
+        L.packinfer_should_regroup.restype = C.c_int32
+        L.packinfer_should_regroup.argtypes = [i32, i64, i32]
+        L.packinfer_append_kv.restype = C.c_int
+        L.packinfer_append_kv.argtypes = [C.POINTER(pi_device_plan), vp, vp, i32, i32, i32, i32, C.c_int, vp, vp, vp]
         L.packinfer_plan_upload.restype = C.c_int
         L.packinfer_plan_upload.argtypes = [C.POINTER(pi_plan), vp, C.c_size_t, vp, C.POINTER(pi_device_plan)]
         L.packinfer_relayout_kv.restype = C.c_int
@@ -174,6 +183,8 @@ class HostPlan:
     def spans(self): return self._view("spans", self.c.n_spans, SPAN_DT)
     @property
     def merges(self): return self._view("merges", self.c.n_merges, MERGE_DT)
+    @property
+    def append_pos(self): return self._view("append_pos", self.c.n_requests, np.dtype("<i4"))
 
 
 def _i32(a) -> np.ndarray:
@@ -181,10 +192,12 @@ def _i32(a) -> np.ndarray:
 
 
 def packinfer_plan(kv_len, q_len, prefix_id=None, prefix_len=(), cfg: Optional[pi_config] = None,
-                   pinned: bool = False, arena=None) -> HostPlan:
-    """Alg. 1 Parts 1-2 + packed execution domain (two-call sizing handled here)."""
+                   pinned: bool = False, arena=None, appended=None) -> HostPlan:
+    """Alg. 1 Parts 1-2 + packed execution domain (two-call sizing handled here).  With `appended`
+    (decode tokens appended per request since the consolidation) this is packinfer_plan_step."""
     L = lib()
     kv, q = _i32(kv_len), _i32(q_len)
+    app = None if appended is None else _i32(appended)
     n = int(kv.shape[0])
     pid = None if prefix_id is None else _i32(prefix_id)
     pl = _i32(prefix_len) if len(prefix_len) else np.zeros(1, np.int32)
@@ -192,12 +205,17 @@ def packinfer_plan(kv_len, q_len, prefix_id=None, prefix_len=(), cfg: Optional[p
     cfg = cfg or default_config()
     out = pi_plan()
     ptr = lambda a: None if a is None else a.ctypes.data
+    def call(a_ptr, a_bytes):
+        if app is None:
+            return L.packinfer_plan(n, ptr(kv), ptr(q), ptr(pid), n_prefix, ptr(pl), C.byref(cfg), a_ptr, a_bytes,
+                                    C.byref(out))
+        return L.packinfer_plan_step(n, ptr(kv), ptr(q), ptr(pid), n_prefix, ptr(pl), ptr(app), C.byref(cfg),
+                                     a_ptr, a_bytes, C.byref(out))
     for _ in range(2):
         if arena is None:
-            st = L.packinfer_plan(n, ptr(kv), ptr(q), ptr(pid), n_prefix, ptr(pl), C.byref(cfg), None, 0, C.byref(out))
+            st = call(None, 0)
         else:
-            st = L.packinfer_plan(n, ptr(kv), ptr(q), ptr(pid), n_prefix, ptr(pl), C.byref(cfg),
-                                  _arena_ptr(arena), _arena_bytes(arena), C.byref(out))
+            st = call(_arena_ptr(arena), _arena_bytes(arena))
         if st == PI_ENOSPC:
             arena = _alloc_arena(int(out.arena_bytes), pinned)
             continue
@@ -279,6 +297,21 @@ def packinfer_attention_decode(dp, q, k_buf, v_buf, out, lse=None, partial_o=Non
                partial_o, partial_lse, gqa_ratio, scale, stream)
 
 
+def packinfer_should_regroup(steps: int, drift: int, capacity: int) -> bool:
+    """Eq. 4 (P:278): t * dL >= C / 2."""
+    return bool(lib().packinfer_should_regroup(int(steps), int(drift), int(capacity)))
+
+
+def packinfer_append_kv(dp: pi_device_plan, k_new, v_new, k_buf, v_buf, hkv_begin: int = 0,
+                        hkv_count: Optional[int] = None, stream=None):
+    """k_new / v_new: [n_requests, Hkv_total, d] — one new decode token per request."""
+    n, hkv_total, d = k_new.shape
+    hkv_count = hkv_total - hkv_begin if hkv_count is None else hkv_count
+    _check(lib().packinfer_append_kv(C.byref(dp), k_new.data_ptr(), v_new.data_ptr(), hkv_total, hkv_begin,
+                                     hkv_count, d, _dt(k_new), k_buf.data_ptr(), v_buf.data_ptr(),
+                                     _stream_ptr(stream)), "packinfer_append_kv")
+
+
 def packinfer_merge(dp, partial_o, partial_lse, out, lse=None, stream=None):
     n_slots, hq, d = partial_o.shape
     _check(lib().packinfer_merge(C.byref(dp), partial_o.data_ptr(), partial_lse.data_ptr(), hq, d, _dt(out),
@@ -316,11 +349,20 @@ class PackedBatch:
         self.partial_o = torch.empty((ns, hq, head_dim), dtype=torch.float32, device=self.device)
         self.partial_lse = torch.empty((ns, hq), dtype=torch.float32, device=self.device)
 
-    def replan(self, stream=None):
-        """Host planning + plan upload (the per-step host part of the hot path)."""
+    def replan(self, stream=None, appended=None):
+        """Host planning + plan upload (the per-step host part of the hot path).  `appended`:
+        decode tokens appended per request since the last consolidation (packinfer_plan_step)."""
         kv_len, q_len, prefix_id, prefix_len = self.args
-        self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, arena=self.plan.arena)
+        self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, arena=self.plan.arena,
+                                   appended=appended)
+        if int(self.plan.c.arena_bytes) > self.dev_arena.numel():
+            import torch
+            self.dev_arena = torch.empty(int(self.plan.c.arena_bytes), dtype=torch.uint8, device=self.device)
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
+
+    def append(self, k_new, v_new, hkv_begin: int = 0, stream=None):
+        """Write one new decode token per request into its headroom slot (current plan)."""
+        packinfer_append_kv(self.dp, k_new, v_new, self.k_buf, self.v_buf, hkv_begin, self.hkv, stream)
 
     def run(self, q, k_paged, v_paged, block_table, out, lse=None, hkv_begin: int = 0, stream=None,
             relayout: bool = True):

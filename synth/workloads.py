@@ -168,7 +168,7 @@ def make_batch(name: str, **kw) -> Batch:
     return CONFIGS[name](**kw)
 
 
-def make_tensors(b: Batch, device="cpu", seed: Optional[int] = None, peaky: float = 1.0):
+def make_tensors(b: Batch, device="cpu", seed: Optional[int] = None, peaky: float = 1.0, extra_tokens: int = 0):
     """Seeded tensors for a batch.
 
     Returns dict with
@@ -176,8 +176,9 @@ def make_tensors(b: Batch, device="cpu", seed: Optional[int] = None, peaky: floa
       k_paged      [num_blocks, page, Hkv, d]
       v_paged      [num_blocks, page, Hkv, d]
       block_table  [n + n_prefix, max_blocks] int32  (rows >= n are the prefixes' tables)
-    Every request's table covers its whole logical sequence; a member of a shared prefix maps
-    the prefix's physical blocks first.  Physical blocks are randomly permuted."""
+    Every request's table covers its whole logical sequence (+ extra_tokens of room for decode
+    appends); a member of a shared prefix maps the prefix's physical blocks first.  Physical blocks
+    are randomly permuted."""
     import torch
     seed = b.seed if seed is None else seed
     P = b.page_size
@@ -189,7 +190,7 @@ def make_tensors(b: Batch, device="cpu", seed: Optional[int] = None, peaky: floa
     own_blocks = []
     for i in range(n):
         base = int(b.prefix_len[b.prefix_id[i]]) if b.prefix_id[i] >= 0 else 0
-        own_blocks.append(-(-(int(b.kv_len[i]) - base) // P))
+        own_blocks.append(-(-(int(b.kv_len[i]) + extra_tokens - base) // P))   # room for decode appends
     nb = sum(pref_blocks) + sum(own_blocks)
     perm = rng.permutation(max(nb, 1)).astype(np.int32)
     cur = 0

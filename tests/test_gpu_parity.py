@@ -189,3 +189,52 @@ def test_full_size_sampled(name):
     assert np.abs(l - rl).max() <= 1e-3
     # property at any size: every row written (finite) exactly
     assert torch.isfinite(out.float()).all()
+
+
+def test_decode_loop_append():
+    """NEXT-1: decode tokens appended into the suffix headroom (no re-consolidation) for up to
+    delta steps, re-planned with packinfer_plan_step; regroup (re-plan + relayout) when the
+    headroom is exhausted or Eq. 4 fires.  Every step matches the oracle on kv_len + k keys."""
+    from paper_2602_06072_b200 import packinfer as pk
+    b = W.random_batch(404, n=12, max_len=700, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    steps, delta, C = 10, 4, 600
+    t = W.make_tensors(b, device="cuda", extra_tokens=steps)
+    r = b.hq // b.hkv
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    kv0 = b.kv_len.copy()
+    mk = lambda kv: pk.PackedBatch(kv, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16, "cuda",
+                                   capacity=C, headroom=delta, decode_chunk=256)
+    pb = mk(kv0)
+    pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], torch.empty_like(t["q"]))
+    bt = t["block_table"].cpu().numpy()
+    appended, since, regroups = 0, 0, 0
+    for k in range(1, steps + 1):
+        # the model produces one new token per request: K/V into the paged cache (engine state, read
+        # by the oracle) and into the group buffer's headroom (packinfer_append_kv)
+        kn = torch.randn((b.n, b.hkv, b.d), generator=g, device="cuda").to(torch.bfloat16)
+        vn = torch.randn((b.n, b.hkv, b.d), generator=g, device="cuda").to(torch.bfloat16)
+        for i in range(b.n):
+            j = int(b.kv_len[i]) + k - 1
+            t["k_paged"][int(bt[i, j // b.page_size]), j % b.page_size] = kn[i]
+            t["v_paged"][int(bt[i, j // b.page_size]), j % b.page_size] = vn[i]
+        q = torch.randn((b.n, b.hq, b.d), generator=g, device="cuda").to(torch.bfloat16)
+        kv_now = b.kv_len + k
+        if appended < delta and not pk.packinfer_should_regroup(since, int(pb.plan.c.drift), C):
+            pb.append(kn, vn)
+            appended += 1
+            since += 1
+            pb.replan(appended=np.full(b.n, appended, np.int32))
+            relayout = False
+        else:                                        # regroup: consolidate kv_len + k from the paged cache
+            pb = mk(kv_now)
+            appended, since, regroups = 0, 0, regroups + 1
+            relayout = True
+        out = torch.full((b.n, b.hq, b.d), float("nan"), dtype=torch.float32, device="cuda")
+        lse = torch.empty((b.hq, b.n), dtype=torch.float32, device="cuda")
+        pb.run(q, t["k_paged"], t["v_paged"], t["block_table"], out, lse, relayout=relayout)
+        torch.cuda.synchronize()
+        ro, rl = OA.attention(q.cpu(), t["k_paged"].cpu(), t["v_paged"].cpu(), t["block_table"].cpu(), kv_now,
+                              b.q_len, b.page_size)
+        H.compare(out, lse, ro, rl)
+    assert regroups >= 1                              # the headroom (4) ran out within 10 steps
