@@ -287,6 +287,7 @@ def main():
     ap.add_argument("--shard", default="group", choices=["group", "heads"])
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-loop", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
@@ -376,6 +377,47 @@ def main():
                             "partial_slots": int(rd.pbs[0].plan.c.n_partial_slots)}
         result["decode"]["gpu_launches"] = rd.launches_per_step * max(3, args.steps)
         del rd
+
+    if not args.no_decode and not args.no_loop:
+        # Decode loop (NEXT-1): consolidate once with headroom delta = 32
+        # (= max new tokens), then each step appends one token per request into its headroom,
+        # re-plans the execution domain on the host (packinfer_plan_step) and runs decode + merge.
+        import torch
+        bd = make_workload("cfg3", 0 if args.shard == "heads" else rank)
+        from synth import workloads as W
+        from paper_2602_06072_b200 import packinfer as pk
+        loop_steps, delta = 32, 32
+        tl = W.make_tensors(bd, device=dev, seed=bd.seed, extra_tokens=loop_steps)
+        rr = bd.hq // bd.hkv
+        pbl = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, rr, bd.d, torch.bfloat16, dev,
+                             headroom=delta)
+        ql = tl["q"][:, h0 * rr:(h0 + hc) * rr]
+        outl = torch.empty((bd.n, hc * rr, bd.d), dtype=torch.bfloat16, device=dev)
+        kn = torch.randn((bd.n, bd.hkv, bd.d), device=dev).to(torch.bfloat16)
+        vn = torch.randn_like(kn)
+        def loop_once():
+            pbl.replan()
+            pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0)   # consolidation
+            for k in range(1, loop_steps):
+                pbl.append(kn, vn, hkv_begin=h0)
+                pbl.replan(appended=np.full(bd.n, k, np.int32))
+                pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0, relayout=False)
+        loop_once()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        loop_once()
+        e1.record()
+        torch.cuda.synchronize()
+        lms = e0.elapsed_time(e1) / loop_steps
+        kv_tokens = sum(int(bd.kv_len.sum()) + k * bd.n for k in range(loop_steps)) / loop_steps
+        lbytes = 2 * kv_tokens * hc * bd.d * 2 + 2 * bd.n * hc * rr * bd.d * 2
+        result.setdefault("decode", {})["loop"] = {
+            "steps": loop_steps, "headroom": delta, "ms_per_step_amortized": lms,
+            "step_gbs_amortized": lbytes / (lms * 1e-3) / 1e9,
+            "note": "consolidation (relayout) once per 32 steps; per step: append + plan_step + upload + "
+                    "decode attention + merge"}
+        del tl, pbl
 
     if not args.no_e2e:
         e_ms, h2d, d2h = e2e_steps(b, runner, max(2, min(args.steps, 5)))

@@ -334,11 +334,18 @@ class PackedBatch:
                                   decode_chunk=decode_chunk, gqa_ratio=gqa_ratio, mem_cap=mem_cap)
         self.args = (kv_len, q_len, prefix_id, prefix_len)
         self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, pinned=True)
+        # Two pinned host arenas alternate: a plan is never rewritten while its asynchronous upload
+        # may still be reading it (each upload records an event; replanning into an arena waits on it).
+        self._arenas = [self.plan.arena, None]
+        self._events = [None, None]
+        self._slot = 0
         self.device = torch.device(device)
         self.hkv, self.r, self.d, self.dtype = hkv_count, gqa_ratio, head_dim, dtype
         c = self.plan.c
         self.dev_arena = torch.empty(max(int(c.arena_bytes), 256), dtype=torch.uint8, device=self.device)
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena)
+        self._events[0] = torch.cuda.Event()
+        self._events[0].record()
         bt = max(int(c.buffer_tokens), 1)
         self.k_buf = torch.empty((hkv_count, bt, head_dim), dtype=dtype, device=self.device)
         # bf16 caches keep V as fp16 in the group buffer (include/packinfer.h)
@@ -352,13 +359,22 @@ class PackedBatch:
     def replan(self, stream=None, appended=None):
         """Host planning + plan upload (the per-step host part of the hot path).  `appended`:
         decode tokens appended per request since the last consolidation (packinfer_plan_step)."""
+        import torch
         kv_len, q_len, prefix_id, prefix_len = self.args
-        self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, arena=self.plan.arena,
+        s = self._slot = 1 - self._slot
+        if self._events[s] is not None:
+            self._events[s].synchronize()          # the upload that last read this arena is done
+        if self._arenas[s] is None:
+            self._arenas[s] = _alloc_arena(int(self.plan.c.arena_bytes), pinned=True)
+        self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, arena=self._arenas[s],
                                    appended=appended)
+        self._arenas[s] = self.plan.arena          # may have grown
         if int(self.plan.c.arena_bytes) > self.dev_arena.numel():
-            import torch
             self.dev_arena = torch.empty(int(self.plan.c.arena_bytes), dtype=torch.uint8, device=self.device)
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream() if stream is None else stream)
+        self._events[s] = ev
 
     def append(self, k_new, v_new, hkv_begin: int = 0, stream=None):
         """Write one new decode token per request into its headroom slot (current plan)."""
