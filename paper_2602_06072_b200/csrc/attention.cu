@@ -65,6 +65,7 @@ struct AttnParams {
   int64_t buffer_tokens;
   unsigned long long* trace;  // debug only (packinfer_debug_trace): CTA-0 clock64 timeline
   int32_t q_heads_stride;  // q_row_stride / head_dim: rows of the 2D (token*stride + head, d) Q view
+  int32_t tiles_per_unit;  // prefill: 2 (GQA head pairs; bf16) or 1 (fp32 operands)
 };
 
 // Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
@@ -96,7 +97,8 @@ struct AttnCfg {
   static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;   // + barriers + alignment slack
   static constexpr uint32_t FMT = F32 ? 2u : 1u;
-  static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 64, 0, 0);   // S in two N=64 halves
+  static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 64, 0, 0);   // decode: S in two N=64 halves
+  static constexpr uint32_t IDESC_QK128 = idesc_make(FMT, 128, 128, 0, 0);  // pair units: one N=128 S
   // bf16: V is the MN-major B operand straight from TMA.  fp32 (kind::tf32): MN-major tf32 needs
   // the 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
   // P is stored as fp16 (10-bit mantissa: 8x smaller rounding than bf16; P <= 2^8 by the lazy
@@ -110,6 +112,7 @@ struct AttnCfg {
   // registers per thread (65536 / THREADS) for the 128-column score row.
   static constexpr int ROLE = 4;
   static constexpr int THREADS = 32 * (ROLE + 8);
+  static constexpr int REG_ROLE = 56, REG_SOFTMAX = 216;   // 128*56 + 256*216 <= 65536
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -121,6 +124,11 @@ enum BarId {
   B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
   B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_COUNT
 };
+
+template <int N>
+__device__ __forceinline__ void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
 
 // Makes the compiler treat r[] as produced after the preceding tcgen05.wait::ld.
 template <int N>
@@ -150,11 +158,12 @@ __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
     u.head0 = k * p.r;
     u.has_b = false;
   } else {
-    const int pairs = (p.r + 1) >> 1;
+    const int tpu = p.tiles_per_unit;
+    const int pairs = (p.r + tpu - 1) / tpu;
     u.kvh = k / pairs;
     const int hp = k % pairs;
-    u.head0 = u.kvh * p.r + 2 * hp;
-    u.has_b = 2 * hp + 1 < p.r;
+    u.head0 = u.kvh * p.r + tpu * hp;
+    u.has_b = tpu == 2 && 2 * hp + 1 < p.r;
   }
   return u;
 }
@@ -202,9 +211,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int total = p.n_work * p.units;
+  // Register budget per warpgroup (setmaxnreg, at the top of each role's branch): the role warps
+  // need few registers, the softmax warps hold a whole 128-column S row.
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
+    reg_dealloc<C::REG_ROLE>();
     // The whole warp walks the schedule (uniform values); one elected lane issues each copy.
     uint32_t t = 0;
     for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
@@ -239,6 +251,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
+    reg_dealloc<C::REG_ROLE>();
     // The whole warp walks the schedule with warp-uniform values (uniform registers); each batch of
     // tcgen05.mma / commit is issued by one elected lane (no per-MMA waterfall loops).
     {
@@ -271,14 +284,28 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         }
         __syncwarp();
       };
+      // S(X) = Q_X K(tt)^T as one N = 128 chain into S/P region X; commits SF[X][0]
+      auto issue_s_full = [&](int X, uint32_t tt) {
+        const uint64_t aq = dq + X * TILE16;
+        const uint64_t bk = dk + (tt % C::NS) * TILE16;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < C::QK_STEPS; ++kk) {
+            const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
+            mma_ss<F32>(tmem + (X ? C::TM_S1 : C::TM_S0), aq + off, bk + off, C::IDESC_QK128, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bar[B_SF00 + 2 * X]);
+        }
+        __syncwarp();
+      };
       auto commit = [&](int id) {
         if (elect_one()) mma_commit(&bar[id]);
         __syncwarp();
       };
-      // O_X += P(region b) V(tt) for keys [64h, 64h + 64)
-      auto issue_pv = [&](int X, int b, uint32_t tt, bool first, int h) {
+      // O_X += P V(tt) for keys [64h, 64h + 64); P starts at TMEM column p_col
+      auto issue_pv = [&](int X, uint32_t p_col, uint32_t tt, bool first, int h) {
         const uint64_t bv = dv + (tt % C::NS) * TILE16;
-        const uint32_t p_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
+        const uint32_t p_tmem = tmem + p_col;
         const uint32_t d_tmem = tmem + (X ? C::TM_O1 : C::TM_O0);
         if (elect_one()) {
 #pragma unroll
@@ -301,9 +328,11 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         trace_unit(p, item, 2);
         tc_fence_after();
         if (u.has_b) {
-          // ---- pair unit: slot X keeps S/P region X; ping-pong between the two tiles
-          issue_s(0, 0, t);
-          issue_s(1, 1, t);
+          // ---- pair unit: slot X keeps S/P region X; ping-pong between the two tiles.  S is one
+          // N = 128 chain (an N = 64 SS MMA is bound by the 128 B/clk shared-memory port: 48 instead
+          // of 32 cycles), P overwrites S's first 64 columns, S(j+1) follows P(j).V in the in-order pipe.
+          issue_s_full(0, t);
+          issue_s_full(1, t);
           commit(B_KFREE0 + (t % C::NS));
           if (n == 1) commit(B_QFREE);
           for (int j = 0; j < n; ++j) {
@@ -315,11 +344,11 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
               if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
               tc_fence_after();
-              issue_pv(X, X, tt, j == 0, 0);
+              issue_pv(X, X ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
               commit(B_PVH0 + X);
               mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
               tc_fence_after();
-              issue_pv(X, X, tt, false, 1);
+              issue_pv(X, X ? C::TM_S1 : C::TM_S0, tt, false, 1);
               trace_ev(p, tt, 14 + X);
               if (X == 1) commit(B_VFREE0 + (tt % C::NS));
               if (j == n - 1) {
@@ -329,7 +358,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                   mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NS)], ((tt + 1) / C::NS) & 1);
                   tc_fence_after();
                 }
-                issue_s(X, X, tt + 1);
+                issue_s_full(X, tt + 1);
                 trace_ev(p, tt, 2 + 3 * X);
                 if (X == 1) {
                   commit(B_KFREE0 + ((tt + 1) % C::NS));
@@ -362,11 +391,11 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
             if (j == 0) mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
             tc_fence_after();
-            issue_pv(0, b, tt, j == 0, 0);
+            issue_pv(0, b ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
             commit(B_PVH0);
             mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
             tc_fence_after();
-            issue_pv(0, b, tt, false, 1);
+            issue_pv(0, b ? C::TM_S1 : C::TM_S0, tt, false, 1);
             commit(B_VFREE0 + (tt % C::NS));
             if (j == n - 1) commit(B_OFULL0);
             if (j + 2 < n) {
@@ -389,6 +418,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     __syncwarp();
   } else if (warp == 2) {
     // ------------------------------------------------------------------ Q gather (TMA tile::gather4)
+    reg_dealloc<C::REG_ROLE>();
     // Q rows are addressed through the plan's row table: lane g gathers rows 4g..4g+3 of each tile
     // (one gather4 per 128-byte atom column) straight into the SWIZZLE_128B K-major operand layout.
     uint32_t item = 0;
@@ -422,6 +452,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     }
   } else if (warp < C::ROLE) {
     // ------------------------------------------------------------------ fp32 only: V^T staging
+    reg_dealloc<C::REG_ROLE>();
     if constexpr (F32) {
       uint32_t t = 0;
       for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
@@ -455,6 +486,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------------ softmax / epilogue
+    reg_alloc<C::REG_SOFTMAX>();
     const int X = (warp - C::ROLE) >> 2;   // tile slot: 0 = A, 1 = B
     const int wq = warp & 3;               // the TMEM lane quarter this warp may access
     const int row_id = wq * 32 + lane;
@@ -500,7 +532,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         for (int k0 = sp.begin; k0 < se; k0 += 128, ++j) {
           const int b = u.has_b ? X : (int)(j & 1);          // S/P region of this tile
           const uint32_t kb = u.has_b ? j : (j >> 1);        // use index of region b in this unit
-          const uint32_t s_tm = tmem + lane_base + (b ? C::TM_S1 : C::TM_S0);
+          const uint32_t region = tmem + lane_base + (b ? C::TM_S1 : C::TM_S0);
           // visible key columns of this row in this tile: [c_lo, c_hi).  Rows past row_count take
           // the full-tile path (their results are discarded) so a warp never diverges on them.
           int c_lo = 0, c_hi = 128;
@@ -520,18 +552,69 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           // (updated only when it grows by > 2^8).  A jump in the first half rescales O before any
           // P of this tile is used; a jump in the second half rescales O after the first half's
           // P.V has landed (O then holds it, so one rescale covers both).
+          uint32_t r[64];
+          auto load_s = [&](uint32_t col) {
+            tmem_ld32(col, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_ld32(col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          };
+          if (row_id == 0) trace_ev(p, t + j, 6 + 4 * X);
+          mbar_wait(&bar[B_SF00 + 2 * b], (cnt[b] + kb) & 1);   // pair units: the whole N = 128 S
+          tc_fence_after();
+          if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
+          if (warp_any) {
+            load_s(region);
+            tmem_wait_ld();
+            reg_fence(r);
+          }
+          // exp2 of the 64 scores in r, packed in place (fp16 pairs into r[0..31]; fp32 stays put)
+          // (use_poly: PI_POLY_PAIRS of 8 pairs on the FMA pipe; clamp: x unbounded, see ex2_poly2)
+          auto exp_body = [&](auto use_poly, auto clamp, uint64_t SL2, uint64_t NM, uint64_t& acc0,
+                              uint64_t& acc1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const uint64_t x = f2_fma(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), SL2, NM);
+              uint64_t e;
+              if (decltype(use_poly)::value && (i & 7) >= 8 - PI_POLY_PAIRS)
+                e = ex2_poly2<decltype(clamp)::value>(x);
+              else
+                e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
+              if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
+              if constexpr (!F32) {
+                r[i] = pack_f16(f2_lo(e), f2_hi(e));      // in place: i <= 2i
+              } else {
+                r[2 * i] = __float_as_uint(f2_lo(e));
+                r[2 * i + 1] = __float_as_uint(f2_hi(e));
+              }
+            }
+          };
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            if (row_id == 0 && h == 0) trace_ev(p, t + j, 6 + 4 * X);
-            mbar_wait(&bar[B_SF00 + 2 * b + h], (cnt[b] + kb) & 1);
-            tc_fence_after();
-            if (row_id == 0 && h == 0) trace_ev(p, t + j, 7 + 4 * X);
             if (warp_any) {
-              uint32_t r[64];
-              tmem_ld32(s_tm + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-              tmem_ld32(s_tm + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-              tmem_wait_ld();
-              reg_fence(r);
+              // Speculative half (unmasked tiles once the running max is set): exponentiate against
+              // m_ref without computing the half's max.  Every P <= 2^8 (the lazy-max invariant)
+              // exactly when no score exceeds m_ref + 8, which the half's sum <= 2^8 certifies;
+              // otherwise (rare) reload S from TMEM and take the exact path below.
+              bool spec_done = false;
+              if constexpr (!F32) {
+                if (__all_sync(0xffffffffu, full && m_ref != NEG_INF)) {   // warp-uniform
+                  uint64_t a0 = 0, a1 = 0;
+                  exp_body(std::true_type{}, std::true_type{}, f2(sl2, sl2), f2(-m_ref, -m_ref), a0, a1);
+                  const uint64_t hs = f2_add(a0, a1);
+                  const float half_sum = f2_lo(hs) + f2_hi(hs);
+                  if (!__any_sync(0xffffffffu, !(half_sum <= 256.0f))) {
+                    ps[0] += f2_lo(a0);
+                    ps[1] += f2_hi(a0);
+                    ps[2] += f2_lo(a1);
+                    ps[3] += f2_hi(a1);
+                    spec_done = true;
+                  } else {
+                    load_s(region + 64u * h);
+                    tmem_wait_ld();
+                    reg_fence(r);
+                  }
+                }
+              }
+              if (!spec_done) {
               if (!full) {
 #pragma unroll
                 for (int i = 0; i < 64; ++i) {
@@ -549,8 +632,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                 const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
                 if (h == 0) {
                   if (j > 0) {
-                    // pair units: P.V(j-1) completed before S(j) did (in-order tcgen05 pipe);
-                    // single-tile units issue P.V(j-1) after S(j): wait for it
+                    // P.V(j-1) must have landed in O: pair units issue S(j) behind it (in-order
+                    // tcgen05 pipe); single-tile units issue it after S(j), so wait
                     if (!u.has_b) {
                       const uint32_t tp = t + j - 1;
                       mbar_wait(&bar[B_VFREE0 + (tp % C::NS)], (tp / C::NS) & 1);
@@ -578,25 +661,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               const float nm = live ? -m_ref : NEG_INF;
               const uint64_t SL2 = f2(sl2, sl2), NM = f2(nm, nm);
               uint64_t acc0 = f2(ps[0], ps[1]), acc1 = f2(ps[2], ps[3]);
-              auto body = [&](auto use_poly) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const uint64_t x =
-                      f2_fma(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), SL2, NM);
-                  uint64_t e;
-                  if (decltype(use_poly)::value && (i & 7) >= 8 - PI_POLY_PAIRS)
-                    e = ex2_poly2(x);
-                  else
-                    e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
-                  if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
-                  if constexpr (!F32) {
-                    r[i] = pack_f16(f2_lo(e), f2_hi(e));      // in place: i <= 2i
-                  } else {
-                    r[2 * i] = __float_as_uint(f2_lo(e));
-                    r[2 * i + 1] = __float_as_uint(f2_hi(e));
-                  }
-                }
-              };
+              auto body = [&](auto use_poly) { exp_body(use_poly, std::false_type{}, SL2, NM, acc0, acc1); };
               if (!F32 && full)
                 body(std::true_type{});
               else
@@ -605,17 +670,33 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               ps[1] = f2_hi(acc0);
               ps[2] = f2_lo(acc1);
               ps[3] = f2_hi(acc1);
-              if constexpr (!F32) {
-                tmem_st32(s_tm + h * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-              } else {
-                tmem_st32(s_tm + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-                tmem_st32(s_tm + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
               }
+              if constexpr (!F32) {
+                tmem_st32(region + h * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              } else {
+                tmem_st32(region + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+                tmem_st32(region + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+              }
+            }
+            if (h == 0) {
+              // load S half 1 before releasing P half 0
+              if (!u.has_b) {
+                mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt[b] + kb) & 1);
+                tc_fence_after();
+              }
+              if (row_id == 0) trace_ev(p, t + j, 16 + 2 * X);
+              if (warp_any) {
+                load_s(region + 64u);
+                tmem_wait_ld();
+                tmem_wait_st();
+                reg_fence(r);
+              }
+            } else if (warp_any) {
               tmem_wait_st();
             }
             tc_fence_before();
             mbar_arrive(&bar[(h == 0 ? B_PHALF0 : B_PFULL0) + b]);
-            if (row_id == 0 && h == 1) trace_ev(p, t + j, 9 + 4 * X);
+            if (row_id == 0) trace_ev(p, t + j, (h == 0 ? 8 : 9) + 4 * X);
           }
           if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
         }
@@ -710,7 +791,10 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
   p.rows = dp->rows;
   p.spans = dp->spans;
   p.n_work = n_work;
-  p.units = decode ? hkv_count : hkv_count * ((r + 1) / 2);
+  // fp32 operands keep one tile per unit: their P fills the whole 128-column S region, which the
+  // pair units' TMEM ring cannot hold
+  p.tiles_per_unit = F32 ? 1 : 2;
+  p.units = decode ? hkv_count : hkv_count * ((r + p.tiles_per_unit - 1) / p.tiles_per_unit);
   p.is_decode = decode ? 1 : 0;
   p.r = r;
   p.q = static_cast<const uint8_t*>(q);

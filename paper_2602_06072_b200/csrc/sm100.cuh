@@ -265,9 +265,17 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
 // 2^x for a pair on the FMA pipe (MUFU offload): x clamped to >= -125, x = n + f with
 // n = rint(x) (1.5*2^23 magic add), f in [-1/2, 1/2], 2^f by a minimax cubic (max rel. err
 // 7.5e-5, well below the bf16 rounding P receives), then n is added to the exponent field.
+// CLAMP_HI also clamps x <= 64 (the result then still flags an overflow as > 2^8): needed when x
+// is not already bounded by a computed maximum, since the exponent add would wrap for x >= 128.
+template <bool CLAMP_HI = false>
 __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
   const float MAGIC = 12582912.0f;
-  const uint64_t xc = f2(fmaxf(f2_lo(x), -125.0f), fmaxf(f2_hi(x), -125.0f));
+  float xl = fmaxf(f2_lo(x), -125.0f), xh = fmaxf(f2_hi(x), -125.0f);
+  if (CLAMP_HI) {
+    xl = fminf(xl, 64.0f);
+    xh = fminf(xh, 64.0f);
+  }
+  const uint64_t xc = f2(xl, xh);
   const uint64_t t = f2_add(xc, f2(MAGIC, MAGIC));
   const uint64_t n = f2_add(t, f2(-MAGIC, -MAGIC));
   const uint64_t f = f2_fma(n, f2(-1.0f, -1.0f), xc);

@@ -21,26 +21,25 @@ A = tr.cpu().numpy().astype(np.int64)
 a = A[:64 * 24].reshape(64, 24)
 U = A[64 * 24:].reshape(64, 8)
 t0 = a[a > 0].min()
-names = ["mA_wait", "mA_got", "mA_iss", "mB_wait", "mB_got", "mB_iss",
-         "sA_wS", "sA_gotS", "sA_p1", "sA_arrP", "sB_wS", "sB_gotS", "sB_p1", "sB_arrP"]
-print("tile " + " ".join(f"{n:>8s}" for n in names))
+names = ["mA_wP", "mA_gotP", "mA_S+", "mB_wP", "mB_gotP", "mB_S+",
+         "sA_wS0", "sA_gS0", "sA_PH", "sA_PF", "sB_wS0", "sB_gS0", "sB_PH", "sB_PF", "mA_PV1", "mB_PV1",
+         "sA_gS1", "sA_-", "sB_gS1"]
+print("tile " + " ".join(f"{n:>7s}" for n in names))
 for i in range(40):
     row = a[i]
-    print(f"{i:4d} " + " ".join(f"{(v - t0 if v else -1):8d}" for v in row[:14]))
-# per-tile durations
-d = lambda x, y: a[:40, y] - a[:40, x]
-print("median sA: waitS", np.median(d(6, 7)), "pass1", np.median(d(7, 8)), "pass2+", np.median(d(8, 9)))
-print("median sB: waitS", np.median(d(10, 11)), "pass1", np.median(d(11, 12)), "pass2+", np.median(d(12, 13)))
-print("median mma: waitPA", np.median(d(0, 1)), "issueA", np.median(d(1, 2)), "waitPB", np.median(d(3, 4)), "issueB", np.median(d(4, 5)))
-print("median A: waitV", np.median(d(1, 16)), "PVissue", np.median(d(16, 14)), "waitK", np.median(d(14, 18)), "Sissue", np.median(d(18, 2)))
-print("median B: waitV", np.median(d(4, 17)), "PVissue", np.median(d(17, 15)), "waitK", np.median(d(15, 19)), "Sissue", np.median(d(19, 5)))
-print("softmax A phases: gotS->ld0", np.median(d(7, 20)), "h0 compute", np.median(d(20, 21)), "->ld1", np.median(d(21, 22)), "h1 compute", np.median(d(22, 23)), "->end", np.median(d(23, 8)))
-print("tile period (A arrive->arrive)", np.median(np.diff(a[:40, 9])))
+    print(f"{i:4d} " + " ".join(f"{(v - t0 if v else -1):7d}" for v in row[:19]))
+d = lambda x, y: a[2:40, y] - a[2:40, x]
+med = lambda x, y: float(np.median(d(x, y)))
+for X, nm in ((0, "A"), (1, "B")):
+    o = 4 * X
+    print(f"softmax {nm}: waitS0 {med(6+o, 7+o):.0f}  h0 {med(7+o, 8+o):.0f}  waitS1 {med(8+o, 16+2*X):.0f}  "
+          f"h1 {med(16+2*X, 9+o):.0f}  period {float(np.median(np.diff(a[2:40, 9+o]))):.0f}")
+    print(f"mma {nm}: PHALF->got {med(0+3*X, 1+3*X):.0f}  got->PV1 issued {med(1+3*X, 14+X):.0f}  PV1->S+ {med(14+X, 2+3*X):.0f}")
+print("S(j+1) issued -> softmax got S0(j+1) A:", float(np.median(a[3:40, 7] - a[2:39, 2])), " B:", float(np.median(a[3:40, 11] - a[2:39, 5])))
+print("PFULL(j) -> S(j+1) issued A:", float(np.median(a[2:40, 2] - a[2:40, 9])), " B:", float(np.median(a[2:40, 5] - a[2:40, 13])))
 
 u0 = U[U > 0].min()
-print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done   (n_ktiles)")
-w = pb.plan.prefill_work
-for i in range(48):
-    r = U[i]
-    item = (0 + i * 148) // 16
-    print(f"{i:4d} " + " ".join(f"{(v - u0 if v else -1):9d}" for v in r[:7]), int(w[item]["n_ktiles"]) if item < len(w) else -1)
+nu = int((U[:, 3] > 0).sum())
+ev = torch.cuda.Event(enable_timing=True); ev2 = torch.cuda.Event(enable_timing=True)
+ev.record(); pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out); ev2.record(); torch.cuda.synchronize()
+print("CTA0 units traced", nu, "cycles first->last", int(U[nu - 1, 3] - u0), "step ms", ev.elapsed_time(ev2))

@@ -93,6 +93,27 @@ def test_peaky_queries():
         H.compare(out, lse, ro, rl)
 
 
+def test_outlier_keys_late():
+    """Keys far above every earlier score appear late in long rows (score jumps of > 128 in log2
+    units): the speculative half (exp against the running max, certified by its sum) must detect
+    the overflow, including on the FMA-pipe exp2 lanes, and fall back to the exact rescale."""
+    b = W.random_batch(91, n=6, max_len=900, hq=8, hkv=2, d=128, n_prefix=0)
+    t = W.make_tensors(b, device="cuda")
+    t["q"] = (t["q"].float() + 0.5).to(t["q"].dtype)          # positive mean: q . 1 ~ 64
+    P = b.page_size
+    bt = t["block_table"].cpu().numpy()
+    for i in range(b.n):
+        L = int(b.kv_len[i])
+        for pos in (L // 3, (2 * L) // 3, L - 2):
+            if pos <= 0:
+                continue
+            blk, slot = int(bt[i, pos // P]), pos % P
+            t["k_paged"][blk, slot, :, :] = 20.0 * (1 + (pos % 5))   # q . k / sqrt(d) >> 128 / log2(e)
+    out, lse, _ = H.run_batch(b, t, C=400, decode_chunk=256, out_f32=True)
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out, lse, ro, rl)
+
+
 def test_mask_probe():
     """q = 0, V channel 0 = request id (exact in bf16): any cross-request leak moves o[0]; exp(lse)
     must count exactly the causally visible keys (pos + 1)."""
