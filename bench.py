@@ -225,6 +225,78 @@ def e2e_steps(b, runner, steps):
     return s.elapsed_time(e) / steps, h2d, d2h
 
 
+def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
+    """BASELINE.json configs[4]: Llama-3-70B-shaped mixed batch (2 x 128k-token prefills split
+    across groups + 30 short prefills + 224 decodes up to 32k), ONE fused attention launch over
+    prefill and decode work items (NEXT-3) + LSE merge; the split form (one launch per kind) is
+    timed beside it on the same plan."""
+    import torch
+    from synth import workloads as W
+    from paper_2602_06072_b200 import packinfer as pk
+    bm = W.cfg5_mixed(3 + (0 if args.shard == "heads" else rank))
+    r = bm.hq // bm.hkv
+    tm = W.make_tensors(bm, device=dev, seed=bm.seed)
+    pbm = pk.PackedBatch(bm.kv_len, bm.q_len, bm.prefix_id, bm.prefix_len, hc, r, bm.d, torch.bfloat16, dev)
+    qm = tm["q"][:, h0 * r:(h0 + hc) * r]
+    outm = torch.empty((bm.total_q, hc * r, bm.d), dtype=torch.bfloat16, device=dev)
+    lsem = torch.empty((hc * r, bm.total_q), dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def once(fused, times):
+        pbm.replan(st)
+        pk.packinfer_relayout_kv(pbm.dp, tm["k_paged"], tm["v_paged"], tm["block_table"], pbm.k_buf, pbm.v_buf,
+                                 h0, hc, st)
+        a, m, e = ev(), ev(), ev()
+        a.record(st)
+        if fused:
+            pk.packinfer_attention(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o, pbm.partial_lse,
+                                   r, 0.0, st)
+            m.record(st)
+        else:
+            pk.packinfer_attention_prefill(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o,
+                                           pbm.partial_lse, r, 0.0, st)
+            m.record(st)
+            pk.packinfer_attention_decode(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o,
+                                          pbm.partial_lse, r, 0.0, st)
+        e.record(st)
+        pk.packinfer_merge(pbm.dp, pbm.partial_o, pbm.partial_lse, outm, lsem, st)
+        times.append((a, m, e))
+
+    steps = 2
+    for fused in (True, False):
+        once(fused, [])
+    torch.cuda.synchronize()
+    res = {}
+    for fused in (True, False):
+        times = []
+        s0, s1 = ev(), ev()
+        s0.record(st)
+        for _ in range(steps):
+            once(fused, times)
+        s1.record(st)
+        torch.cuda.synchronize()
+        res[fused] = (s0.elapsed_time(s1) / steps, sum(a.elapsed_time(e) for a, _, e in times) / steps,
+                      sum(a.elapsed_time(m) for a, m, _ in times) / steps)
+    step_ms, fused_ms, _ = res[True]
+    _, split_ms, split_pre_ms = res[False]
+    flops = 4 * bm.d * hc * r * sum(q * (L - q) + q * (q + 1) // 2
+                                    for L, q in zip(bm.kv_len.tolist(), bm.q_len.tolist()) if q > 1)
+    c = pbm.plan.c
+    out = {"workload": bm.name + " (BASELINE.json configs[4])", "requests": bm.n,
+           "prefill_tokens": int(bm.q_len[bm.q_len > 1].sum()), "decode_requests": int((bm.q_len == 1).sum()),
+           "hq": bm.hq, "hkv": bm.hkv, "groups": int(c.n_groups), "prefill_items": int(c.n_prefill_work),
+           "decode_items": int(c.n_decode_work), "partial_slots": int(c.n_partial_slots),
+           "prefill_tflop": flops / 1e12, "ms_per_step": step_ms,
+           "fused_attention_ms": fused_ms, "split_attention_ms": split_ms, "split_prefill_ms": split_pre_ms,
+           "tflops_fused": flops / (fused_ms * 1e-3) / 1e12,
+           "frac_fused": flops / (fused_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+           "note": "tflops_fused counts prefill FLOPs only over the fused (prefill + decode) kernel time",
+           "gpu_launches": 4 * steps}
+    del tm, pbm
+    return out
+
+
 # ------------------------------------------------------------------------------- oracle timing
 def oracle_sample(b, budget_s: float, seed: int):
     """Times the oracle (as it stands) on a bounded sample of the workload's requests on this
@@ -289,6 +361,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-loop", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-mixed", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -418,6 +491,9 @@ def main():
             "note": "consolidation (relayout) once per 32 steps; per step: append + plan_step + upload + "
                     "decode attention + merge"}
         del tl, pbl
+
+    if not args.no_mixed:
+        result["mixed"] = mixed_section(dev, h0, hc, rank, args, peaks, dist_on)
 
     if not args.no_e2e:
         e_ms, h2d, d2h = e2e_steps(b, runner, max(2, min(args.steps, 5)))

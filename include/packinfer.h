@@ -227,8 +227,8 @@ PI_API pi_status packinfer_append_kv(const pi_device_plan* dp, const void* k_new
  * Packed attention ("union of valid query-key regions"; P:172 one launch for every
  * group): ONE persistent launch over all prefill (resp. decode) work items x local heads.
  * S = scale * Q K^T and O += P V run on tcgen05 (TMEM accumulators, TMA-fed K/V), softmax is
- * online with fp32 statistics; bf16 inputs, fp32 accumulation, P rounded to bf16 (reading
- * R13; PI_FP32 uses kind::tf32).  q/out: local heads [0, hkv_count*gqa_ratio) of each token
+ * online with fp32 statistics; bf16 Q/K, fp32 accumulation, P rounded to fp16 against the fp16
+ * V of the group buffers (reading R13; PI_FP32 uses kind::tf32).  q/out: local heads [0, hkv_count*gqa_ratio) of each token
  * (strides in elements); rows with a single result write out/lse directly, split rows write
  * (o, lse) to partial slots for packinfer_merge.  head_dim in {64, 128}.
  * lse may be NULL.  softmax_scale <= 0 selects 1/sqrt(head_dim).
@@ -245,6 +245,18 @@ PI_API pi_status packinfer_attention_decode(const pi_device_plan* dp, const void
                                      const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,
                                      int32_t head_dim, float softmax_scale, pi_dtype dt,
                                      void* out, int64_t out_row_stride, float* lse,
+                                     float* partial_o, float* partial_lse, pi_stream_t stream);
+
+/* Fused form (NEXT-3; BASELINE.json north star "one packed attention kernel launch
+ * per layer ... covering both prefill and decode"): ONE persistent launch over the prefill AND
+ * the decode work items of the plan (prefill units first, the cheaper decode units fill the
+ * tail).  Arguments, layouts and errors as above; q/out hold every request's rows (q_len = 1
+ * for decode requests) in the caller's varlen order.  Equivalent to
+ * packinfer_attention_prefill followed by packinfer_attention_decode.                         */
+PI_API pi_status packinfer_attention(const pi_device_plan* dp, const void* q, int64_t q_row_stride,
+                                     const void* k_buf, const void* v_buf, int32_t hkv_count,
+                                     int32_t gqa_ratio, int32_t head_dim, float softmax_scale,
+                                     pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
                                      float* partial_o, float* partial_lse, pi_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------

@@ -43,12 +43,14 @@ namespace pi {
 using namespace sm100;
 
 struct AttnParams {
-  const pi_work* work;
+  const pi_work* work_p;   // prefill work items (units [0, total_p))
+  const pi_work* work_d;   // decode work items (units [total_p, total_p + n_work_d * units_d))
   const pi_row* rows;
   const pi_span* spans;
-  int32_t n_work;
-  int32_t units;      // launch units per item: hkv * ceil(r/2) (prefill) or hkv (decode)
-  int32_t is_decode;
+  int32_t n_work_p, n_work_d;
+  int32_t units_p;    // launch units per prefill item: hkv * ceil(r / tiles_per_unit)
+  int32_t units_d;    // launch units per decode item: hkv
+  int32_t total_p;    // n_work_p * units_p
   int32_t r;          // GQA ratio
   const uint8_t* q;
   int64_t q_row_stride;    // elements
@@ -149,15 +151,20 @@ struct Unit {
 // within ~1% on the BASELINE.json batches without any inter-CTA communication.
 __device__ __forceinline__ int snake_unit(int k, int b, int G) { return k * G + ((k & 1) ? (G - 1 - b) : b); }
 
+// Unit w: prefill units first (each list is sorted by cost, descending), then decode units, so
+// the cheap decode units fill the tail of the one persistent launch (NEXT-3).
 __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
   Unit u;
-  u.wk = p.work[w / p.units];
-  const int k = w % p.units;
-  if (p.is_decode) {
+  if (w >= p.total_p) {
+    w -= p.total_p;
+    u.wk = p.work_d[w / p.units_d];
+    const int k = w % p.units_d;
     u.kvh = k;
     u.head0 = k * p.r;
     u.has_b = false;
   } else {
+    u.wk = p.work_p[w / p.units_p];
+    const int k = w % p.units_p;
     const int tpu = p.tiles_per_unit;
     const int pairs = (p.r + tpu - 1) / tpu;
     u.kvh = k / pairs;
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int total = p.n_work * p.units;
+  const int total = p.total_p + p.n_work_d * p.units_d;
   // Register budget per warpgroup (setmaxnreg, at the top of each role's branch): the role warps
   // need few registers, the softmax warps hold a whole 128-column S row.
 
@@ -493,6 +500,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t o_tm = tmem + lane_base + (X ? C::TM_O1 : C::TM_O0);
     uint32_t cnt[2] = {0, 0}, ix = 0, t = 0;
+    // completions so far of SF[b][1] (S half 1 of region b): only single-tile units compute S in
+    // two halves; pair units' one N = 128 chain completes SF[X][0] alone
+    uint32_t cnt1[2] = {0, 0};
     uint32_t pvh = 0;                       // completions so far of PVH[X] (this slot's P.V halves)
     const float NEG_INF = -INFINITY;
     const float sl2 = p.scale_log2;
@@ -516,6 +526,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       if (X == 1 && !u.has_b) {            // slot B idles; keep the region counters in step
         cnt[0] += (n + 1) >> 1;
         cnt[1] += n >> 1;
+        cnt1[0] += (n + 1) >> 1;
+        cnt1[1] += n >> 1;
         t += n;
         continue;
       }
@@ -596,12 +608,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               // otherwise (rare) reload S from TMEM and take the exact path below.
               bool spec_done = false;
               if constexpr (!F32) {
-                if (__all_sync(0xffffffffu, full && m_ref != NEG_INF)) {   // warp-uniform
+                // warp-uniform, decided by the valid rows only: rows past row_count hold stale Q
+                // rows of an earlier unit (their results are discarded) and must not steer it
+                if (__all_sync(0xffffffffu, !valid || (full && m_ref != NEG_INF))) {
                   uint64_t a0 = 0, a1 = 0;
                   exp_body(std::true_type{}, std::true_type{}, f2(sl2, sl2), f2(-m_ref, -m_ref), a0, a1);
                   const uint64_t hs = f2_add(a0, a1);
                   const float half_sum = f2_lo(hs) + f2_hi(hs);
-                  if (!__any_sync(0xffffffffu, !(half_sum <= 256.0f))) {
+                  if (!__any_sync(0xffffffffu, valid && !(half_sum <= 256.0f))) {
                     ps[0] += f2_lo(a0);
                     ps[1] += f2_hi(a0);
                     ps[2] += f2_lo(a1);
@@ -681,7 +695,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             if (h == 0) {
               // load S half 1 before releasing P half 0
               if (!u.has_b) {
-                mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt[b] + kb) & 1);
+                mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt1[b] + kb) & 1);
                 tc_fence_after();
               }
               if (row_id == 0) trace_ev(p, t + j, 16 + 2 * X);
@@ -762,6 +776,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       } else {
         cnt[0] += (n + 1) >> 1;
         cnt[1] += n >> 1;
+        cnt1[0] += (n + 1) >> 1;
+        cnt1[1] += n >> 1;
       }
       pvh += n;
       t += n;
@@ -778,24 +794,26 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
 
 unsigned long long* g_debug_trace = nullptr;
 
+// mode: bit 0 = prefill work items, bit 1 = decode work items (both = one fused launch)
 template <int D, bool F32>
-static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, const void* q, int64_t q_row_stride,
+static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const void* q, int64_t q_row_stride,
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                         cudaStream_t stream) {
   using C = AttnCfg<D, F32>;
-  const int32_t n_work = decode ? dp->n_decode_work : dp->n_prefill_work;
-  if (n_work == 0) return PI_OK;
   AttnParams p{};
-  p.work = decode ? dp->decode_work : dp->prefill_work;
+  p.work_p = dp->prefill_work;
+  p.work_d = dp->decode_work;
+  p.n_work_p = (mode & 1) ? dp->n_prefill_work : 0;
+  p.n_work_d = (mode & 2) ? dp->n_decode_work : 0;
+  if (p.n_work_p + p.n_work_d == 0) return PI_OK;
   p.rows = dp->rows;
   p.spans = dp->spans;
-  p.n_work = n_work;
-  // fp32 operands keep one tile per unit: their P fills the whole 128-column S region, which the
-  // pair units' TMEM ring cannot hold
+  // fp32 operands keep one tile per unit: their P fills the whole 128-column S region
   p.tiles_per_unit = F32 ? 1 : 2;
-  p.units = decode ? hkv_count : hkv_count * ((r + p.tiles_per_unit - 1) / p.tiles_per_unit);
-  p.is_decode = decode ? 1 : 0;
+  p.units_p = hkv_count * ((r + p.tiles_per_unit - 1) / p.tiles_per_unit);
+  p.units_d = hkv_count;
+  p.total_p = p.n_work_p * p.units_p;
   p.r = r;
   p.q = static_cast<const uint8_t*>(q);
   p.q_row_stride = q_row_stride;
@@ -839,19 +857,20 @@ static pi_status launch(const pi_device_plan* dp, bool decode, bool out_f32, con
     if (s != PI_OK) return s;
     attr_set = true;
   }
-  const int64_t total = (int64_t)n_work * p.units;
+  const int64_t total = (int64_t)p.total_p + (int64_t)p.n_work_d * p.units_d;
   const int grid = (int)std::min<int64_t>(total, num_sms());
   packed_attention_kernel<D, F32><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ);
   return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
 }
 
-static pi_status attention_entry(bool decode, const pi_device_plan* dp, const void* q, int64_t q_row_stride,
+static pi_status attention_entry(int mode, const pi_device_plan* dp, const void* q, int64_t q_row_stride,
                                  const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,
                                  int32_t head_dim, float softmax_scale, pi_dtype dt, void* out,
                                  int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                                  pi_stream_t stream) {
   if (!dp) return fail(PI_EINVAL, "device plan is NULL");
-  const int32_t n_work = decode ? dp->n_decode_work : dp->n_prefill_work;
+  const bool decode = (mode & 2) && dp->n_decode_work > 0;
+  const int32_t n_work = ((mode & 1) ? dp->n_prefill_work : 0) + ((mode & 2) ? dp->n_decode_work : 0);
   if (n_work == 0) return ok();
   if (!q || !k_buf || !v_buf || !out) return fail(PI_EINVAL, "q, k_buf, v_buf and out must be non-NULL");
   if (hkv_count < 1 || gqa_ratio < 1 || gqa_ratio > 16) return fail(PI_EINVAL, "bad hkv_count / gqa_ratio");
@@ -877,13 +896,13 @@ static pi_status attention_entry(bool decode, const pi_device_plan* dp, const vo
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)head_dim);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dt == PI_BF16 && head_dim == 128)
-    s = launch<128, false>(dp, decode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+    s = launch<128, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                            out_row_stride, lse, partial_o, partial_lse, st);
   else if (dt == PI_BF16 && head_dim == 64)
-    s = launch<64, false>(dp, decode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+    s = launch<64, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                           out_row_stride, lse, partial_o, partial_lse, st);
   else
-    s = launch<64, true>(dp, decode, false, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+    s = launch<64, true>(dp, mode, false, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                          out_row_stride, lse, partial_o, partial_lse, st);
   return s == PI_OK ? ok() : s;
 }
@@ -901,7 +920,7 @@ pi_status packinfer_attention_prefill(const pi_device_plan* dp, const void* q, i
                                       int32_t head_dim, float softmax_scale, pi_dtype dt, void* out,
                                       int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                                       pi_stream_t stream) {
-  return pi::attention_entry(false, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim,
+  return pi::attention_entry(1, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim,
                              softmax_scale, dt, out, out_row_stride, lse, partial_o, partial_lse, stream);
 }
 
@@ -910,8 +929,16 @@ pi_status packinfer_attention_decode(const pi_device_plan* dp, const void* q, in
                                      int32_t head_dim, float softmax_scale, pi_dtype dt, void* out,
                                      int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                                      pi_stream_t stream) {
-  return pi::attention_entry(true, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim,
+  return pi::attention_entry(2, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim,
                              softmax_scale, dt, out, out_row_stride, lse, partial_o, partial_lse, stream);
+}
+
+pi_status packinfer_attention(const pi_device_plan* dp, const void* q, int64_t q_row_stride, const void* k_buf,
+                              const void* v_buf, int32_t hkv_count, int32_t gqa_ratio, int32_t head_dim,
+                              float softmax_scale, pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
+                              float* partial_o, float* partial_lse, pi_stream_t stream) {
+  return pi::attention_entry(3, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim, softmax_scale,
+                             dt, out, out_row_stride, lse, partial_o, partial_lse, stream);
 }
 
 }  // extern "C"

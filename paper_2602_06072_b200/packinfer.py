@@ -28,7 +28,7 @@ PI_BF16, PI_FP32, PI_BF16_OUT_F32 = 0, 1, 2
 EXPORTS = [
     "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
     "packinfer_plan", "packinfer_plan_upload", "packinfer_relayout_kv",
-    "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_merge",
+    "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_attention", "packinfer_merge",
     "packinfer_plan_step", "packinfer_should_regroup", "packinfer_append_kv",
 ]
 
@@ -121,7 +121,7 @@ def lib():
         L.packinfer_relayout_kv.restype = C.c_int
         L.packinfer_relayout_kv.argtypes = [C.POINTER(pi_device_plan), vp, vp, vp, i32, i32, i32, i32, i32, i32,
                                             C.c_int, vp, vp, vp]
-        for name in ("packinfer_attention_prefill", "packinfer_attention_decode"):
+        for name in ("packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_attention"):
             f = getattr(L, name)
             f.restype = C.c_int
             f.argtypes = [C.POINTER(pi_device_plan), vp, i64, vp, vp, i32, i32, i32, f32, C.c_int, vp, i64, vp,
@@ -297,6 +297,13 @@ def packinfer_attention_decode(dp, q, k_buf, v_buf, out, lse=None, partial_o=Non
                partial_o, partial_lse, gqa_ratio, scale, stream)
 
 
+def packinfer_attention(dp, q, k_buf, v_buf, out, lse=None, partial_o=None, partial_lse=None,
+                        gqa_ratio: int = 1, scale: float = 0.0, stream=None):
+    """Fused: one launch over the plan's prefill and decode work items (include/packinfer.h)."""
+    _attention("packinfer_attention", "packinfer_attention", dp, q, k_buf, v_buf, out, lse,
+               partial_o, partial_lse, gqa_ratio, scale, stream)
+
+
 def packinfer_should_regroup(steps: int, drift: int, capacity: int) -> bool:
     """Eq. 4 (P:278): t * dL >= C / 2."""
     return bool(lib().packinfer_should_regroup(int(steps), int(drift), int(capacity)))
@@ -381,12 +388,18 @@ class PackedBatch:
         packinfer_append_kv(self.dp, k_new, v_new, self.k_buf, self.v_buf, hkv_begin, self.hkv, stream)
 
     def run(self, q, k_paged, v_paged, block_table, out, lse=None, hkv_begin: int = 0, stream=None,
-            relayout: bool = True):
+            relayout: bool = True, fused: bool = True):
+        """relayout -> attention -> merge.  fused: ONE attention launch over prefill and decode work
+        items (packinfer_attention); else one launch per kind (prefill, then decode)."""
         if relayout:
             packinfer_relayout_kv(self.dp, k_paged, v_paged, block_table, self.k_buf, self.v_buf,
                                   hkv_begin, self.hkv, stream)
-        packinfer_attention_prefill(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
-                                    self.partial_lse, self.r, 0.0, stream)
-        packinfer_attention_decode(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
-                                   self.partial_lse, self.r, 0.0, stream)
+        if fused:
+            packinfer_attention(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
+                                self.partial_lse, self.r, 0.0, stream)
+        else:
+            packinfer_attention_prefill(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
+                                        self.partial_lse, self.r, 0.0, stream)
+            packinfer_attention_decode(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
+                                       self.partial_lse, self.r, 0.0, stream)
         packinfer_merge(self.dp, self.partial_o, self.partial_lse, out, lse, stream)

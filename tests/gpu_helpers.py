@@ -16,8 +16,9 @@ ATOL_MEAN = 1e-3  # north star: mean-abs <= 1e-3
 
 
 def run_batch(b, t, C=8192, delta=0, decode_chunk=1024, num_groups=0, hkv_begin=0, hkv_count=None,
-              relayout=True, out_f32=False):
-    """Runs plan -> upload -> relayout -> prefill -> decode -> merge on cuda:0.
+              relayout=True, out_f32=False, fused=True):
+    """Runs plan -> upload -> relayout -> attention (one fused launch, or prefill + decode launches)
+    -> merge on cuda:0.
     t: tensors on cuda (from synth.make_tensors).  Returns (out, lse, PackedBatch)."""
     r = b.hq // b.hkv
     hkv_count = b.hkv - hkv_begin if hkv_count is None else hkv_count
@@ -28,7 +29,9 @@ def run_batch(b, t, C=8192, delta=0, decode_chunk=1024, num_groups=0, hkv_begin=
     out = torch.full((b.total_q, hkv_count * r, b.d), float("nan"), dtype=torch.float32 if out_f32 else dt,
                      device="cuda")
     lse = torch.full((hkv_count * r, b.total_q), float("nan"), dtype=torch.float32, device="cuda")
-    pb.run(q, t["k_paged"], t["v_paged"], t["block_table"], out, lse, hkv_begin=hkv_begin)
+    pb.partial_o.fill_(float("nan"))        # every partial slot the merge reads must be written
+    pb.partial_lse.fill_(float("nan"))
+    pb.run(q, t["k_paged"], t["v_paged"], t["block_table"], out, lse, hkv_begin=hkv_begin, fused=fused)
     torch.cuda.synchronize()
     return out, lse, pb
 

@@ -93,6 +93,34 @@ def test_peaky_queries():
         H.compare(out, lse, ro, rl)
 
 
+@pytest.mark.parametrize("seed", [5, 6])
+def test_fused_launch_equals_split(seed):
+    """NEXT-3: one launch over prefill + decode work items computes, unit for unit, what the two
+    separate launches compute (bitwise), and matches the oracle."""
+    b = W.random_batch(seed, n=16, max_len=900, hq=8, hkv=2, d=128, decode_frac=0.5)
+    assert (b.q_len == 1).any() and (b.q_len > 1).any()
+    t = W.make_tensors(b, device="cuda")
+    out_f, lse_f, _ = H.run_batch(b, t, C=512, decode_chunk=256, fused=True)
+    out_s, lse_s, _ = H.run_batch(b, t, C=512, decode_chunk=256, fused=False)
+    assert torch.equal(out_f, out_s)
+    dl = (lse_f != lse_s).nonzero()
+    assert dl.numel() == 0, (dl[:8].tolist(), lse_f[tuple(dl[:8].T)].tolist(), lse_s[tuple(dl[:8].T)].tolist())
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out_f, lse_f, ro, rl)
+    H.compare(out_s, lse_s, ro, rl)
+
+
+@pytest.mark.parametrize("hq,hkv", [(6, 2), (2, 1), (5, 1)])
+def test_odd_gqa_ratio_mixed_units(hq, hkv):
+    """r = 3 (or 5) leaves a single-tile unit beside each head pair in prefill, and the fused launch
+    mixes pair and single units on every CTA: the per-region barrier phases must stay in step."""
+    b = W.random_batch(40 + hq, n=12, max_len=700, hq=hq, hkv=hkv, d=128, decode_frac=0.4)
+    t = W.make_tensors(b, device="cuda")
+    out, lse, _ = H.run_batch(b, t, C=384, decode_chunk=256)
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out, lse, ro, rl)
+
+
 def test_outlier_keys_late():
     """Keys far above every earlier score appear late in long rows (score jumps of > 128 in log2
     units): the speculative half (exp against the running max, certified by its sum) must detect
