@@ -432,6 +432,29 @@ def main():
               "roofline": roofline, "clocks": clocks,
               "gpu_launches": runner.launches_per_step * args.steps}
 
+    if dist_on and args.shard == "heads":
+        # Full O on every rank (only for callers that need it; not part of the timed step): one
+        # NCCL all-gather of the head-sharded outputs over NVLink.
+        from paper_2602_06072_b200 import shard
+        import torch.distributed as dist
+        shard.gather_heads(runner.out, world, b.hkv, runner.r)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        g0.record()
+        for _ in range(reps):
+            full = shard.gather_heads(runner.out, world, b.hkv, runner.r)
+        g1.record()
+        torch.cuda.synchronize()
+        gt = torch.tensor([g0.elapsed_time(g1) / reps], device=dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gbytes = full.numel() * full.element_size()
+        result["gather"] = {"ms": float(gt[0]), "bytes_out": gbytes,
+                            "step_ms_with_gather": ms_step + float(gt[0]),
+                            "note": "NCCL all_gather_into_tensor of head-major O slabs + layout copy"}
+        del full
+
     if not args.no_decode:
         bd = make_workload("cfg3", 0 if args.shard == "heads" else rank)
         rd = Runner(bd, dev, h0, hc, seed=bd.seed)

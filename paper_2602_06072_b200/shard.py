@@ -7,6 +7,8 @@ The path shards without communication:
   * Group sharding: groups (Alg. 1 S_g) are assigned to ranks by LPT on their cost, so each rank
     consolidates and attends only its groups' KV (weak scaling over independent groups/batches).
 No collective is on the data path; `plan_digest` lets ranks assert they planned identically.
+A caller that needs the full O on every rank gathers the head shards once per step
+(`gather_heads`: one all-gather over NCCL / NVLink).
 """
 
 from __future__ import annotations
@@ -51,3 +53,25 @@ def plan_digest(host_plan) -> str:
     arena = host_plan.arena
     raw = bytes(arena.numpy().tobytes() if hasattr(arena, "numpy") else bytes(arena))
     return hashlib.sha256(raw[: int(c.arena_bytes)]).hexdigest()
+
+
+def gather_heads(out_local, world: int, hkv_total: int, gqa_ratio: int, group=None):
+    """All-gather of KV-head-sharded outputs (SURVEY 8(e) "gather outputs where a caller needs
+    them").  out_local: [T, count_r * gqa_ratio, d] of this rank (kv_head_shard order); returns
+    the full [T, hkv_total * gqa_ratio, d] on every rank.  Shards travel as head-major slabs
+    [heads, T, d] padded to the largest shard, so one all_gather_into_tensor (NCCL) moves them."""
+    import torch
+    import torch.distributed as dist
+    counts = [kv_head_shard(hkv_total, q, world)[1] for q in range(world)]
+    hmax = max(counts) * gqa_ratio
+    T, hl, d = out_local.shape
+    slab = out_local.new_zeros((hmax, T, d))
+    if hl:
+        slab[:hl] = out_local.transpose(0, 1)
+    gathered = out_local.new_empty((world, hmax, T, d))
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, slab, group=group)
+    else:
+        dist.all_gather(list(gathered.unbind(0)), slab, group=group)
+    parts = [gathered[q, :counts[q] * gqa_ratio] for q in range(world)]
+    return torch.cat(parts, 0).transpose(0, 1).contiguous()

@@ -47,6 +47,12 @@ def _worker(rank, world, port, q):
             loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(world)]
             # LPT bound: max load <= mean + largest group
             res[name + "_balance"] = max(loads) <= sum(loads) / world + max(costs)
+        # output all-gather of KV-head shards (hkv = 5 does not divide evenly: padded slabs)
+        g = torch.Generator().manual_seed(3)
+        full = torch.randn((37, 5 * 4, 16), generator=g)
+        b0, c0 = shard.kv_head_shard(5, rank, world)
+        got = shard.gather_heads(full[:, b0 * 4:(b0 + c0) * 4].contiguous(), world, 5, 4)
+        res["gather_equal"] = bool(torch.equal(got, full))
         hb, hc = shard.kv_head_shard(8, rank, world)
         heads = [None] * world
         dist.all_gather_object(heads, list(range(hb, hb + hc)))
@@ -79,6 +85,7 @@ def test_two_rank_gloo():
             assert res[name + "_owner_equal"], name
             assert res[name + "_balance"], name
         assert res["heads"] == list(range(8))
+        assert res["gather_equal"]
         assert res["tmax"] == 2.0
 
 
