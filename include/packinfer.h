@@ -94,7 +94,15 @@ typedef struct {
   int32_t tile_k;       /* keys per K tile; must be 128 (P:159 T in {128,256})               */
   int32_t decode_chunk; /* max keys per decode work item (multiple of tile_k; e.g. 1024)      */
   int32_t gqa_ratio;    /* r = Hq / Hkv in [1, 16]: decode rows are (request, GQA head)       */
+  int32_t flags;        /* PI_PLAN_* bits; 0 = the method.  (Occupies the struct's former tail
+                           padding: sizeof(pi_config) is unchanged.)                           */
 } pi_config;
+
+/* Ablation (NEXT-4; Fig. "breakdown" P:480-489): every request's query rows start
+ * their own 128-row tiles (no packing of short requests into shared tiles) - the
+ * "unpacked compute" baseline.  Groups, layout and results are unchanged; only tile count and
+ * tile efficiency change.                                                                     */
+#define PI_PLAN_NO_QPACK 1
 
 /* Fill *cfg with the defaults: C=8192, G auto, no M_max, delta=0, 128/128 tiles,
  * decode_chunk=1024, gqa_ratio=1. */

@@ -66,6 +66,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const int32_t r = cfg->gqa_ratio;
   const int32_t TQ = cfg->tile_q, TK = cfg->tile_k;
   const int64_t chunk = cfg->decode_chunk;
+  const bool no_qpack = (cfg->flags & PI_PLAN_NO_QPACK) != 0;
   if (C < 1) return fail(PI_EINVAL, "capacity must be >= 1");
   if (delta < 0 || cfg->num_groups < 0 || cfg->mem_cap < 0)
     return fail(PI_EINVAL, "negative headroom / num_groups / mem_cap");
@@ -74,6 +75,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   if (TQ != 128 || TK != 128) return fail(PI_EINVAL, "tile_q and tile_k must be 128");
   if (chunk < TK || chunk % TK) return fail(PI_EINVAL, "decode_chunk must be a positive multiple of tile_k");
   if (r < 1 || r > 16) return fail(PI_EINVAL, "gqa_ratio must be in [1, 16]");
+  if (cfg->flags & ~PI_PLAN_NO_QPACK) return fail(PI_EINVAL, "unknown pi_config.flags bits");
   int64_t total_q = 0;
   for (int32_t i = 0; i < n; ++i) {
     const int32_t L = kv_len[i], q = q_len[i];
@@ -303,7 +305,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       if (a0 >= a1) { close_tile(); continue; }       // piece holds no query rows
       const int32_t nrows = a1 - a0;
       const bool split = first_piece[i + 1] - first_piece[i] > 1;
-      if (split || nrows >= TQ) {
+      if (split || nrows >= TQ || no_qpack) {
         close_tile();
         for (int32_t c = a0; c < a1; c += TQ)
           emit_tile(g, e.ctx, {{e.piece, {c, std::min(a1, c + TQ)}}});

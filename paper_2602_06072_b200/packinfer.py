@@ -43,7 +43,10 @@ class PackInferError(RuntimeError):
 class pi_config(C.Structure):
     _fields_ = [("capacity", C.c_int32), ("num_groups", C.c_int32), ("mem_cap", C.c_int64),
                 ("headroom", C.c_int32), ("tile_q", C.c_int32), ("tile_k", C.c_int32),
-                ("decode_chunk", C.c_int32), ("gqa_ratio", C.c_int32)]
+                ("decode_chunk", C.c_int32), ("gqa_ratio", C.c_int32), ("flags", C.c_int32)]
+
+
+PI_PLAN_NO_QPACK = 1   # ablation: one Q tile set per request (include/packinfer.h)
 
 
 PIECE_DT = np.dtype([("request", "<i4"), ("piece", "<i4"), ("kv_begin", "<i4"), ("kv_len", "<i4"), ("group", "<i4")])
