@@ -35,7 +35,7 @@
 #include "sm100.cuh"
 
 #ifndef PI_POLY_PAIRS
-#define PI_POLY_PAIRS 3   // of every 8 score pairs, this many take exp2 on the FMA pipe
+#define PI_POLY_PAIRS 2   // of every 8 score pairs, this many take exp2 on the FMA pipe (A/B: scripts/ab_poly.sh)
 #endif
 
 namespace pi {
