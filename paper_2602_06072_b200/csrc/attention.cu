@@ -97,7 +97,11 @@ struct AttnCfg {
   static constexpr int OFF_K = 2 * TILE_BYTES;
   static constexpr int OFF_V = OFF_K + NS * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;   // + barriers + alignment slack
+  static constexpr int OFF_XCH = OFF_BAR + 256;       // single units: (m, l) of both warpgroups
+  static constexpr int SMEM = OFF_XCH + 2 * 128 * 8 + 1024;   // + alignment slack
+  // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
+  // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
+  static constexpr uint32_t P1_SINGLE = F32 ? 64u : 96u;
   static constexpr uint32_t FMT = F32 ? 2u : 1u;
   static constexpr uint32_t IDESC_QK = idesc_make(FMT, 128, 64, 0, 0);   // decode: S in two N=64 halves
   static constexpr uint32_t IDESC_QK128 = idesc_make(FMT, 128, 128, 0, 0);  // pair units: one N=128 S
@@ -126,6 +130,10 @@ enum BarId {
   B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
   B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_COUNT
 };
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 template <int N>
 __device__ __forceinline__ void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
@@ -309,7 +317,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         if (elect_one()) mma_commit(&bar[id]);
         __syncwarp();
       };
-      // O_X += P V(tt) for keys [64h, 64h + 64); P starts at TMEM column p_col
+      // O_X += P_h V(tt)[keys 64h .. 64h+63]; P_h (this half's P) starts at TMEM column p_col;
+      // first: overwrite O_X instead of accumulating
       auto issue_pv = [&](int X, uint32_t p_col, uint32_t tt, bool first, int h) {
         const uint64_t bv = dv + (tt % C::NS) * TILE16;
         const uint32_t p_tmem = tmem + p_col;
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             const int kk = h * (C::PV_STEPS / 2) + q;
             const uint64_t off = F32 ? (uint64_t)(((kk >> 2) * C::VT_ATOM_BYTES + (kk & 3) * 32) >> 4)
                                      : (uint64_t)((kk * C::KEYS_PER_PV_STEP * 128) >> 4);
-            mma_ts<F32>(d_tmem, p_tmem + kk * 8, bv + off, C::IDESC_PV, (first && kk == 0) ? 0u : 1u);
+            mma_ts<F32>(d_tmem, p_tmem + q * 8, bv + off, C::IDESC_PV, (first && q == 0) ? 0u : 1u);
           }
         }
         __syncwarp();
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               commit(B_PVH0 + X);
               mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
               tc_fence_after();
-              issue_pv(X, X ? C::TM_S1 : C::TM_S0, tt, false, 1);
+              issue_pv(X, (X ? C::TM_S1 : C::TM_S0) + 32, tt, false, 1);
               trace_ev(p, tt, 14 + X);
               if (X == 1) commit(B_VFREE0 + (tt % C::NS));
               if (j == n - 1) {
@@ -396,15 +405,23 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             mbar_wait(&bar[B_PHALF0 + b], (cnt[b] + (j >> 1)) & 1);
             trace_ev(p, tt, 1);
             mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
-            if (j == 0) mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
+            if (j == 0) {
+              mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
+              mbar_wait(&bar[B_OFREE1], (ix[1] & 1) ^ 1);
+            }
             tc_fence_after();
+            // split-K inside the CTA: keys 0..63 of every tile -> O_0 (softmax warpgroup A),
+            // keys 64..127 -> O_1 (warpgroup B); the epilogue merges the two (LSE)
             issue_pv(0, b ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
             commit(B_PVH0);
             mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
             tc_fence_after();
-            issue_pv(0, b ? C::TM_S1 : C::TM_S0, tt, false, 1);
+            issue_pv(1, (b ? C::TM_S1 : C::TM_S0) + C::P1_SINGLE, tt, j == 0, 1);
             commit(B_VFREE0 + (tt % C::NS));
-            if (j == n - 1) commit(B_OFULL0);
+            if (j == n - 1) {
+              commit(B_OFULL0);
+              commit(B_OFULL1);
+            }
             if (j + 2 < n) {
               mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NS)], ((tt + 2) / C::NS) & 1);
               tc_fence_after();
@@ -416,6 +433,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           cnt[0] += (n + 1) >> 1;
           cnt[1] += n >> 1;
           ix[0] += 1;
+          ix[1] += 1;
         }
         trace_unit(p, item, 3);
         t += n;
@@ -523,14 +541,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       const Unit u = get_unit(p, w);
       const pi_work& wk = u.wk;
       const int n = wk.n_ktiles;
-      if (X == 1 && !u.has_b) {            // slot B idles; keep the region counters in step
-        cnt[0] += (n + 1) >> 1;
-        cnt[1] += n >> 1;
-        cnt1[0] += (n + 1) >> 1;
-        cnt1[1] += n >> 1;
-        t += n;
-        continue;
-      }
+      // pair units: warpgroup X owns tile X (both key halves); single-tile units: warpgroup X owns
+      // key half X of every tile (split-K inside the CTA, merged in the epilogue)
+      const int h_lo = u.has_b ? 0 : X, h_hi = u.has_b ? 2 : X + 1;
       const bool valid = row_id < wk.row_count;
       const bool warp_any = wq * 32 < wk.row_count;
       pi_row row = {0, 0, 0, 0};
@@ -570,11 +583,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             tmem_ld32(col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           };
           if (row_id == 0) trace_ev(p, t + j, 6 + 4 * X);
-          mbar_wait(&bar[B_SF00 + 2 * b], (cnt[b] + kb) & 1);   // pair units: the whole N = 128 S
+          if (u.has_b || X == 0)
+            mbar_wait(&bar[B_SF00 + 2 * b], (cnt[b] + kb) & 1);   // pair units: the whole N = 128 S
+          else
+            mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt1[b] + kb) & 1);
           tc_fence_after();
           if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
           if (warp_any) {
-            load_s(region);
+            load_s(region + 64u * h_lo);
             tmem_wait_ld();
             reg_fence(r);
           }
@@ -601,6 +617,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           };
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (h < h_lo || h >= h_hi) continue;
+            // the first half this warpgroup handles in this tile (single units: its only one)
+            const bool first_half = !u.has_b || h == 0;
             if (warp_any) {
               // Speculative half (unmasked tiles once the running max is set): exponentiate against
               // m_ref without computing the half's max.  Every P <= 2^8 (the lazy-max invariant)
@@ -644,7 +663,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
               if (__any_sync(0xffffffffu, need)) {
                 const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
-                if (h == 0) {
+                if (first_half) {
                   if (j > 0) {
                     // P.V(j-1) must have landed in O: pair units issue S(j) behind it (in-order
                     // tcgen05 pipe); single-tile units issue it after S(j), so wait
@@ -686,18 +705,18 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               ps[3] = f2_hi(acc1);
               }
               if constexpr (!F32) {
-                tmem_st32(region + h * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+                // pair units: P_h at 32h (over S columns already read); single units: warpgroup
+                // B's P goes over its own S columns (P1_SINGLE), never over warpgroup A's
+                const uint32_t p_col = u.has_b ? 32u * h : (h ? C::P1_SINGLE : 0u);
+                tmem_st32(region + p_col, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
               } else {
                 tmem_st32(region + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
                 tmem_st32(region + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
               }
             }
-            if (h == 0) {
-              // load S half 1 before releasing P half 0
-              if (!u.has_b) {
-                mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt1[b] + kb) & 1);
-                tc_fence_after();
-              }
+            if (u.has_b && h == 0) {
+              // pair units: load S half 1 (same N = 128 chain, already complete) before releasing
+              // P half 0
               if (row_id == 0) trace_ev(p, t + j, 16 + 2 * X);
               if (warp_any) {
                 load_s(region + 64u);
@@ -718,17 +737,55 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       // ---------------- epilogue: O / l -> out (or partial), lse
       mbar_wait(&bar[B_OFULL0 + X], ix & 1);
       tc_fence_after();
-      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-      const float lse_v = l > 0.f ? (m_ref + __log2f(l)) * 0.69314718055994530942f : NEG_INF;
       const int slot = (row.out >> 4) - 1;
-      const int head = u.head0 + X + (row.out & 15);
+      const int head = u.head0 + (u.has_b ? X : 0) + (row.out & 15);
+      // pair units: out = O_X / l.  Single units: the two warpgroups hold (m, l) of key halves
+      // 0..63 / 64..127 of every tile with partial accumulators O_0 / O_1; merge them (reading
+      // R10: M = max, w = 2^(m - M), L = sum w l) and let warpgroup X write output columns
+      // [X D/2, (X+1) D/2).
+      float sc0, sc1 = 0.f, lse_v;
+      int c4_begin = 0, c4_end = D / 32;
+      if (u.has_b) {
+        sc0 = l > 0.f ? 1.0f / l : 0.f;
+        lse_v = l > 0.f ? (m_ref + __log2f(l)) * 0.69314718055994530942f : NEG_INF;
+      } else {
+        float2* xch = reinterpret_cast<float2*>(smem + C::OFF_XCH);
+        xch[X * 128 + row_id] = make_float2(m_ref, l);
+        named_bar_sync(1, 256);
+        const float2 o = xch[(1 - X) * 128 + row_id];
+        const float mA = X ? o.x : m_ref, lA = X ? o.y : l, mB = X ? m_ref : o.x, lB = X ? l : o.y;
+        const float M = fmaxf(lA > 0.f ? mA : NEG_INF, lB > 0.f ? mB : NEG_INF);
+        const float wA = lA > 0.f ? ex2(mA - M) : 0.f, wB = lB > 0.f ? ex2(mB - M) : 0.f;
+        const float L = lA * wA + lB * wB;
+        const float inv = L > 0.f ? 1.0f / L : 0.f;
+        sc0 = wA * inv;
+        sc1 = wB * inv;
+        lse_v = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
+        c4_begin = X * (D / 64);
+        c4_end = c4_begin + D / 64;
+      }
+      const uint32_t o0_tm = u.has_b ? o_tm : tmem + lane_base + C::TM_O0;
+      const uint32_t o1_tm = tmem + lane_base + C::TM_O1;
       if (warp_any) {
 #pragma unroll
         for (int c4 = 0; c4 < D / 32; ++c4) {
+          if (c4 < c4_begin || c4 >= c4_end) continue;
           uint32_t o32[32];
-          tmem_ld32(o_tm + c4 * 32, o32);
+          tmem_ld32(o0_tm + c4 * 32, o32);
           tmem_wait_ld();
           reg_fence(o32);
+          if (!u.has_b) {
+            uint32_t o1[32];
+            tmem_ld32(o1_tm + c4 * 32, o1);
+            tmem_wait_ld();
+            reg_fence(o1);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              o32[i] = __float_as_uint(fmaf(__uint_as_float(o32[i]), sc0, __uint_as_float(o1[i]) * sc1));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o32[i] = __float_as_uint(__uint_as_float(o32[i]) * sc0);
+          }
           if (valid) {
             if (slot < 0) {
               const int oes = (F32 || p.out_f32) ? 4 : 2;
@@ -739,31 +796,31 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                   uint32_t pk[4];
 #pragma unroll
                   for (int e = 0; e < 4; ++e)
-                    pk[e] = pack_bf16(__uint_as_float(o32[v * 8 + 2 * e]) * inv_l,
-                                      __uint_as_float(o32[v * 8 + 2 * e + 1]) * inv_l);
+                    pk[e] = pack_bf16(__uint_as_float(o32[v * 8 + 2 * e]), __uint_as_float(o32[v * 8 + 2 * e + 1]));
                   reinterpret_cast<uint4*>(dst)[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
               } else {
 #pragma unroll
                 for (int v = 0; v < 8; ++v)
                   reinterpret_cast<float4*>(dst)[v] =
-                      make_float4(__uint_as_float(o32[4 * v]) * inv_l, __uint_as_float(o32[4 * v + 1]) * inv_l,
-                                  __uint_as_float(o32[4 * v + 2]) * inv_l, __uint_as_float(o32[4 * v + 3]) * inv_l);
+                      make_float4(__uint_as_float(o32[4 * v]), __uint_as_float(o32[4 * v + 1]),
+                                  __uint_as_float(o32[4 * v + 2]), __uint_as_float(o32[4 * v + 3]));
               }
             } else {
               float* dst = p.partial_o + ((int64_t)slot * p.hq_count + head) * D + c4 * 32;
 #pragma unroll
               for (int v = 0; v < 8; ++v)
                 reinterpret_cast<float4*>(dst)[v] =
-                    make_float4(__uint_as_float(o32[4 * v]) * inv_l, __uint_as_float(o32[4 * v + 1]) * inv_l,
-                                __uint_as_float(o32[4 * v + 2]) * inv_l, __uint_as_float(o32[4 * v + 3]) * inv_l);
+                    make_float4(__uint_as_float(o32[4 * v]), __uint_as_float(o32[4 * v + 1]),
+                                __uint_as_float(o32[4 * v + 2]), __uint_as_float(o32[4 * v + 3]));
             }
           }
         }
       }
       tc_fence_before();
+      if (!u.has_b) named_bar_sync(1, 256);   // both warpgroups are done with O_0, O_1 and xch
       mbar_arrive(&bar[B_OFREE0 + X]);
-      if (valid) {
+      if (valid && (u.has_b || X == 0)) {
         if (slot < 0) {
           if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
         } else {
@@ -779,7 +836,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         cnt1[0] += (n + 1) >> 1;
         cnt1[1] += n >> 1;
       }
-      pvh += n;
+      if (u.has_b || X == 0) pvh += n;   // PVH1 completes for pair units only
       t += n;
       ++ix;
     }
