@@ -594,6 +594,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             tmem_wait_ld();
             reg_fence(r);
           }
+          if (row_id == 0) trace_ev(p, t + j, 20 + X);
+          uint32_t spec_bits = 0;
           // exp2 of the 64 scores in r, packed in place (fp16 pairs into r[0..31]; fp32 stays put)
           // (use_poly: PI_POLY_PAIRS of 8 pairs on the FMA pipe; clamp: x unbounded, see ex2_poly2)
           auto exp_body = [&](auto use_poly, auto clamp, uint64_t SL2, uint64_t NM, uint64_t& acc0,
@@ -704,6 +706,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               ps[2] = f2_lo(acc1);
               ps[3] = f2_hi(acc1);
               }
+              if (row_id == 0 && h == 0) trace_ev(p, t + j, 22 + X);
+              if (p.trace != nullptr) spec_bits |= (spec_done ? 1u : 0u) << h;
+              if (row_id == 0 && h == 1 && p.trace != nullptr && blockIdx.x == 0 && t + j < (uint32_t)TRACE_TILES)
+                p.trace[(t + j) * 24 + 17 + 2 * X] = spec_bits;
               if constexpr (!F32) {
                 // pair units: P_h at 32h (over S columns already read); single units: warpgroup
                 // B's P goes over its own S columns (P1_SINGLE), never over warpgroup A's

@@ -33,10 +33,20 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, float* sink, unsigned
         uint32_t y;
         asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(y) : "r"(v[i]), "r"(v[(i + 1) & 7]));
         v[i] = y;
-      } else {
+      } else if (MODE == 4) {
         uint32_t y;
         asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(v[i]));
         v[i] = y;
+      } else if (MODE == 5) {
+        // packed fp32x2 FMA on (v[i], v[i^1]) pairs
+        uint64_t a = ((uint64_t)v[i ^ 1] << 32) | v[i], y;
+        asm volatile("fma.rn.f32x2 %0, %1, %1, %1;" : "=l"(y) : "l"(a));
+        v[i] = (uint32_t)y;
+        v[i ^ 1] = (uint32_t)(y >> 32);
+      } else {
+        float y;
+        asm volatile("fma.rn.f32 %0, %1, %1, %1;" : "=f"(y) : "f"(__uint_as_float(v[i])));
+        v[i] = __float_as_uint(y);
       }
     }
   }
@@ -79,6 +89,8 @@ int main() {
     run<4>("ex2.approx.ftz.bf16x2", sms, th, 2);
     run<2>("cvt.rn.f16x2.f32", sms, th, 1);
     run<3>("add.rn.f16x2", sms, th, 2);
+    run<5>("fma.rn.f32x2", sms, th, 2);
+    run<6>("fma.rn.f32", sms, th, 1);
   }
   return 0;
 }

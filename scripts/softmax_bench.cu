@@ -1,0 +1,108 @@
+// Microbenchmark: cycles per 64-column softmax half (the exp2 body of packed_attention_kernel:
+// FFMA2 argument, exp2 split MUFU / FMA-pipe cubic, FADD2 row sum, fp16 pack) with 1 or 2 warps
+// per SMSP, for several formulations.  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2602_06072_b200/csrc scripts/softmax_bench.cu -o scripts/softmax_bench
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+#include "sm100.cuh"
+
+using namespace pi::sm100;
+
+// MODE 0: spec body (poly pairs with clamp), 1: exact body (poly, no upper clamp), 2: all MUFU,
+// 3: all MUFU with scalar FFMA / FADD, 4: all MUFU, no sum, 5: all MUFU, no pack
+template <int MODE, int POLY>
+__global__ void __launch_bounds__(256, 1) bench(int iters, const float* in, unsigned long long* out, float* sink) {
+  uint32_t r[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) r[i] = __float_as_uint(in[(threadIdx.x * 7 + i) & 1023]);
+  const float sl2 = 0.1275f, m = 3.0f;
+  const uint64_t SL2 = f2(sl2, sl2), NM = f2(-m, -m);
+  float tot = 0.f;
+  __syncwarp();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    uint32_t o[32];
+    uint64_t acc0 = 0, acc1 = 0;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      uint64_t e;
+      if (MODE == 6) { o[i] = r[2 * i] ^ r[2 * i + 1]; continue; }
+      if (MODE == 3) {
+        const float xl = fmaf(__uint_as_float(r[2 * i]), sl2, -m), xh = fmaf(__uint_as_float(r[2 * i + 1]), sl2, -m);
+        const float el = ex2(xl), eh = ex2(xh);
+        if (i & 1) s1 += el + eh; else s0 += el + eh;
+        o[i] = pack_f16(el, eh);
+        continue;
+      }
+      const uint64_t x = f2_fma(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), SL2, NM);
+      if (MODE <= 1 && (i & 7) >= 8 - POLY)
+        e = ex2_poly2<MODE == 0>(x);
+      else
+        e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
+      if (MODE != 4) {
+        if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
+      }
+      if (MODE != 5) o[i] = pack_f16(f2_lo(e), f2_hi(e));
+      else o[i] = (uint32_t)e ^ (uint32_t)(e >> 32);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) asm volatile("" ::"r"(o[i]));
+    const uint64_t hs = f2_add(acc0, acc1);
+    tot += f2_lo(hs) + f2_hi(hs) + s0 + s1;
+    // perturb the inputs (packed adds, 32 per half: subtract the "perturb only" line)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      uint64_t v = f2_add(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), f2(1e-6f, 1e-6f));
+      r[2 * i] = __float_as_uint(f2_lo(v));
+      r[2 * i + 1] = __float_as_uint(f2_hi(v));
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x % 32 == 0) out[blockIdx.x * 8 + threadIdx.x / 32] = (unsigned long long)(t1 - t0);
+  if (tot == 1.2345f) sink[0] = tot;
+}
+
+template <int MODE, int POLY>
+void run(const char* name, int sms, int warps, const float* in) {
+  unsigned long long* d;
+  float* sink;
+  cudaMalloc(&d, sms * 8 * 8);
+  cudaMalloc(&sink, 4);
+  const int iters = 4096;
+  bench<MODE, POLY><<<sms, warps * 32>>>(iters, in, d, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148 * 8];
+  cudaMemcpy(h, d, sms * 8 * 8, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += h[i * 8];
+  avg /= sms;
+  printf("%-34s warps/SM=%d: %.0f cycles per 64-column half per warp  err=%s\n", name, warps, avg / iters,
+         cudaGetErrorString(e));
+  cudaFree(d);
+  cudaFree(sink);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float* in;
+  cudaMalloc(&in, 1024 * 4);
+  float h[1024];
+  for (int i = 0; i < 1024; ++i) h[i] = (float)((i * 37) % 101) * 0.1f - 5.0f;
+  cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+  for (int w : {4, 8}) {
+    run<0, 2>("spec body (poly 2/8, clamp)", sms, w, in);
+    run<1, 2>("exact body (poly 2/8)", sms, w, in);
+    run<1, 0>("exact body (poly 0/8)", sms, w, in);
+    run<1, 4>("exact body (poly 4/8)", sms, w, in);
+    run<2, 0>("all MUFU", sms, w, in);
+    run<3, 0>("all MUFU scalar FFMA/FADD", sms, w, in);
+    run<4, 0>("all MUFU, no row sum", sms, w, in);
+    run<5, 0>("all MUFU, no fp16 pack", sms, w, in);
+    run<6, 0>("perturb only (baseline)", sms, w, in);
+  }
+  return 0;
+}

@@ -34,10 +34,13 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* o
 #pragma unroll
         for (int b = 0; b < BATCH; ++b) tmem_ld32(base + b * 32, r[b]);
         tmem_wait_ld();
+        // consume without a dependent arithmetic chain (a serial FADD chain over the 32 values
+        // would take ~4 cycles per value and hide the load rate)
 #pragma unroll
         for (int b = 0; b < BATCH; ++b)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[b][i]);
+          for (int i = 0; i < 32; ++i) asm volatile("" ::"r"(r[b][i]));
+        acc += __uint_as_float(r[0][0]);
       }
     }
   }

@@ -43,3 +43,9 @@ nu = int((U[:, 3] > 0).sum())
 ev = torch.cuda.Event(enable_timing=True); ev2 = torch.cuda.Event(enable_timing=True)
 ev.record(); pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out); ev2.record(); torch.cuda.synchronize()
 print("CTA0 units traced", nu, "cycles first->last", int(U[nu - 1, 3] - u0), "step ms", ev.elapsed_time(ev2))
+for X, nm in ((0, "A"), (1, "B")):
+    o = 4 * X
+    print(f"softmax {nm} detail: ld h0 {med(7+o, 20+X):.0f}  exp h0 {med(20+X, 22+X):.0f}  store+ {med(22+X, 16+2*X):.0f}  "
+          f"ldS1+arrive {med(16+2*X, 8+o):.0f}  h1 {med(8+o, 9+o):.0f}")
+    fl = a[2:40, 17 + 2 * X]
+    print(f"  spec flags (bit0 h0 spec, bit1 h1 spec): {np.bincount((fl & 3).astype(int), minlength=4).tolist()}")
