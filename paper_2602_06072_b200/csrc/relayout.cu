@@ -3,9 +3,10 @@
 // Gathers every copy-plan entry from the paged KV cache [num_blocks, page, Hkv, d] into the
 // group-contiguous buffers [hkv_count, buffer_tokens, d].  For bf16 caches V is stored as fp16
 // (exact for |v| < 65504, saturated beyond) so that the packed attention can multiply an fp16 P
-// (8x finer than bf16) with it; K is copied bitwise.  One warp per buffer token: it reads
-// the token's hkv_count*d contiguous elements (all local heads of one paged slot: coalesced) and
-// scatters them into the per-head buffers.  Cells in a suffix's headroom (delta) are
+// (8x finer than bf16) with it; K is copied bitwise.  One warp per RL_TPW consecutive buffer
+// tokens (one 32-ary search for their copy entry): per token it reads the hkv_count*d contiguous
+// elements of all local heads of one paged slot (coalesced) and scatters them into the per-head
+// buffers.  Cells in a suffix's headroom (delta) are
 // written with zeros so every buffer cell is finite (the attention kernels read whole 128-key
 // tiles; masked keys meet P = 0, which must not multiply NaN garbage).
 // HBM-bound: algorithmic bytes = 2 (K,V) x copied tokens x hkv_count x d x elem (read + write).
@@ -52,54 +53,81 @@ __device__ __forceinline__ uint4 bf16x8_to_f16x8(uint4 v) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-__global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
-  const int64_t g = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (g >= p.total) return;
-  // copy entry containing buffer cell g: largest c with ext_prefix[c] <= g
-  int lo = 0, hi = p.n_copies - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&p.ext_prefix[mid]) <= g) lo = mid; else hi = mid - 1;
+#ifndef PI_RL_TPW
+#define PI_RL_TPW 1
+#endif
+constexpr int RL_TPW = PI_RL_TPW;   // consecutive buffer tokens per warp (one copy-entry search)
+constexpr int RL_U = 4;             // 16-byte chunks per lane in flight per tensor
+
+// Largest c with ext_prefix[c] <= g (ext_prefix strictly increasing, ext_prefix[0] = 0 <= g):
+// 32-ary warp search, each round narrows [lo, hi] ~32x with one coalesced probe per lane, so the
+// dependent-load chain is log32(n_copies) deep instead of log2.
+__device__ __forceinline__ int find_copy(const int64_t* __restrict__ ext_prefix, int n, int64_t g, int lane) {
+  int lo = 0, hi = n - 1;
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    const int c = lo + (int)((span * (lane + 1) + 31) / 32);   // lane 31 probes hi
+    const bool le = __ldg(&ext_prefix[c]) <= g;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    const int k = __popc(m);                                   // probes are monotone: a prefix is true
+    const int c_prev = k > 0 ? lo + (int)((span * k + 31) / 32) : lo;
+    const int c_next = k < 32 ? lo + (int)((span * (k + 1) + 31) / 32) - 1 : hi;
+    lo = c_prev;
+    hi = c_next;
   }
-  const pi_copy cp = p.copies[lo];
-  const int64_t off = g - p.ext_prefix[lo];
-  const int64_t dst = cp.dst + off;
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
+  const int64_t g0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RL_TPW;
+  const int lane = threadIdx.x & 31;
+  if (g0 >= p.total) return;
+  int c = find_copy(p.ext_prefix, p.n_copies, g0, lane);
+  int64_t next = c + 1 < p.n_copies ? __ldg(&p.ext_prefix[c + 1]) : INT64_MAX;
   const int64_t row_bytes = (int64_t)p.head_chunks * 16;
-  constexpr int U = 8;  // up to 8 x 16 B per lane in flight per tensor
-  if (off < cp.len) {
-    const int row = cp.src_kind == 0 ? cp.src_id : p.n_requests + cp.src_id;
-    const int64_t j = cp.src_begin + off;
-    const int blk = __ldg(&p.bt[(int64_t)row * p.max_blocks + j / p.page]);
-    const int64_t src = ((int64_t)blk * p.page + j % p.page) * p.token_bytes + p.head_off_bytes;
-    for (int base = 0; base < p.chunks; base += 32 * U) {
-      uint4 kv[U], vv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * 32 + lane;
-        if (i < p.chunks) {
-          kv[u] = __ldg(reinterpret_cast<const uint4*>(p.kp + src) + i);
-          vv[u] = __ldg(reinterpret_cast<const uint4*>(p.vp + src) + i);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * 32 + lane;
-        if (i < p.chunks) {
-          const int h = i / p.head_chunks, c = i % p.head_chunks;
-          const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)c * 16;
-          *reinterpret_cast<uint4*>(p.kb + d) = kv[u];
-          *reinterpret_cast<uint4*>(p.vb + d) = p.v_to_f16 ? bf16x8_to_f16x8(vv[u]) : vv[u];
-        }
-      }
+  const int64_t g_end = min(g0 + RL_TPW, p.total);
+  for (int64_t g = g0; g < g_end; ++g) {
+    while (g >= next) {   // next copy entry (copies are long: rarely taken)
+      ++c;
+      next = c + 1 < p.n_copies ? __ldg(&p.ext_prefix[c + 1]) : INT64_MAX;
     }
-  } else {
-    const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int i = lane; i < p.chunks; i += 32) {
-      const int h = i / p.head_chunks, c = i % p.head_chunks;
-      const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)c * 16;
-      *reinterpret_cast<uint4*>(p.kb + d) = z;
-      *reinterpret_cast<uint4*>(p.vb + d) = z;
+    const pi_copy cp = p.copies[c];
+    const int64_t off = g - __ldg(&p.ext_prefix[c]);
+    const int64_t dst = cp.dst + off;
+    if (off < cp.len) {
+      const int row = cp.src_kind == 0 ? cp.src_id : p.n_requests + cp.src_id;
+      const int64_t j = cp.src_begin + off;
+      const int blk = __ldg(&p.bt[(int64_t)row * p.max_blocks + j / p.page]);
+      const int64_t src = ((int64_t)blk * p.page + j % p.page) * p.token_bytes + p.head_off_bytes;
+      for (int base = 0; base < p.chunks; base += 32 * RL_U) {
+        uint4 kv[RL_U], vv[RL_U];
+#pragma unroll
+        for (int u = 0; u < RL_U; ++u) {
+          const int i = base + u * 32 + lane;
+          if (i < p.chunks) {
+            kv[u] = __ldg(reinterpret_cast<const uint4*>(p.kp + src) + i);
+            vv[u] = __ldg(reinterpret_cast<const uint4*>(p.vp + src) + i);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RL_U; ++u) {
+          const int i = base + u * 32 + lane;
+          if (i < p.chunks) {
+            const int h = i / p.head_chunks, cc = i % p.head_chunks;
+            const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)cc * 16;
+            *reinterpret_cast<uint4*>(p.kb + d) = kv[u];
+            *reinterpret_cast<uint4*>(p.vb + d) = p.v_to_f16 ? bf16x8_to_f16x8(vv[u]) : vv[u];
+          }
+        }
+      }
+    } else {
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (int i = lane; i < p.chunks; i += 32) {
+        const int h = i / p.head_chunks, cc = i % p.head_chunks;
+        const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)cc * 16;
+        *reinterpret_cast<uint4*>(p.kb + d) = z;
+        *reinterpret_cast<uint4*>(p.vb + d) = z;
+      }
     }
   }
 }
@@ -196,7 +224,7 @@ extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void*
   p.kb = static_cast<uint8_t*>(k_buf);
   p.vb = static_cast<uint8_t*>(v_buf);
   p.v_to_f16 = dt == PI_BF16 ? 1 : 0;
-  const int64_t blocks = (p.total + 7) / 8;
+  const int64_t blocks = (p.total + 8 * RL_TPW - 1) / (8 * RL_TPW);
   if (blocks > 0x7fffffff) return fail(PI_EINVAL, "buffer too large");
   relayout_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   pi_status s = cuda_check(cudaGetLastError(), "relayout_kernel launch");
