@@ -13,7 +13,7 @@ using namespace pi::sm100;
 // MODE 0: spec body (poly pairs with clamp), 1: exact body (poly, no upper clamp), 2: all MUFU,
 // 3: all MUFU with scalar FFMA / FADD, 4: all MUFU, no sum, 5: all MUFU, no pack
 template <int MODE, int POLY>
-__global__ void __launch_bounds__(256, 1) bench(int iters, const float* in, unsigned long long* out, float* sink) {
+__global__ void __launch_bounds__(512, 1) bench(int iters, const float* in, unsigned long long* out, float* sink) {
   uint32_t r[64];
 #pragma unroll
   for (int i = 0; i < 64; ++i) r[i] = __float_as_uint(in[(threadIdx.x * 7 + i) & 1023]);
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, const float* in, unsi
     }
   }
   const long long t1 = clock64();
-  if (threadIdx.x % 32 == 0) out[blockIdx.x * 8 + threadIdx.x / 32] = (unsigned long long)(t1 - t0);
+  if (threadIdx.x % 32 == 0) out[blockIdx.x * 16 + threadIdx.x / 32] = (unsigned long long)(t1 - t0);
   if (tot == 1.2345f) sink[0] = tot;
 }
 
@@ -69,15 +69,15 @@ template <int MODE, int POLY>
 void run(const char* name, int sms, int warps, const float* in) {
   unsigned long long* d;
   float* sink;
-  cudaMalloc(&d, sms * 8 * 8);
+  cudaMalloc(&d, sms * 16 * 8);
   cudaMalloc(&sink, 4);
   const int iters = 4096;
   bench<MODE, POLY><<<sms, warps * 32>>>(iters, in, d, sink);
   cudaError_t e = cudaDeviceSynchronize();
-  unsigned long long h[148 * 8];
-  cudaMemcpy(h, d, sms * 8 * 8, cudaMemcpyDeviceToHost);
+  unsigned long long h[148 * 16];
+  cudaMemcpy(h, d, sms * 16 * 8, cudaMemcpyDeviceToHost);
   double avg = 0;
-  for (int i = 0; i < sms; ++i) avg += h[i * 8];
+  for (int i = 0; i < sms; ++i) avg += h[i * 16];
   avg /= sms;
   printf("%-34s warps/SM=%d: %.0f cycles per 64-column half per warp  err=%s\n", name, warps, avg / iters,
          cudaGetErrorString(e));
@@ -93,7 +93,7 @@ int main() {
   float h[1024];
   for (int i = 0; i < 1024; ++i) h[i] = (float)((i * 37) % 101) * 0.1f - 5.0f;
   cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
-  for (int w : {4, 8}) {
+  for (int w : {4, 8, 16}) {
     run<0, 2>("spec body (poly 2/8, clamp)", sms, w, in);
     run<1, 2>("exact body (poly 2/8)", sms, w, in);
     run<1, 0>("exact body (poly 0/8)", sms, w, in);

@@ -9,7 +9,7 @@
 using namespace pi::sm100;
 
 template <int WARPS, int BATCH, bool STORE>
-__global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* out, float* sink) {
+__global__ void __launch_bounds__(512, 1) bench(int iters, unsigned long long* out, float* sink) {
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32;
   if (warp == 0) tmem_alloc<512>(&tslot);
@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* o
   float acc = 0.f;
   long long t0 = clock64();
   if (warp < WARPS) {
-    const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >= 4 ? 256 : 0);
+    const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + ((warp >> 2) & 3) * 128;
     for (int it = 0; it < iters; ++it) {
       if (STORE) {
         uint32_t r[32];
@@ -63,7 +63,7 @@ void run(int sms) {
   cudaMalloc(&d, sms * 8);
   cudaMalloc(&sink, 4);
   const int iters = 2048;
-  bench<WARPS, BATCH, STORE><<<sms, 256>>>(iters, d, sink);
+  bench<WARPS, BATCH, STORE><<<sms, 512>>>(iters, d, sink);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[256];
   cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
@@ -85,6 +85,8 @@ int main() {
   run<4, 4, false>(sms);
   run<8, 1, false>(sms);
   run<8, 2, false>(sms);
+  run<16, 1, false>(sms);
+  run<16, 2, false>(sms);
   run<4, 1, true>(sms);
   run<4, 2, true>(sms);
   run<8, 2, true>(sms);
