@@ -12,7 +12,7 @@ using namespace pi::sm100;
 
 // MODE 0: spec body (poly pairs with clamp), 1: exact body (poly, no upper clamp), 2: all MUFU,
 // 3: all MUFU with scalar FFMA / FADD, 4: all MUFU, no sum, 5: all MUFU, no pack
-template <int MODE, int POLY>
+template <int MODE, int POLY, bool SERIAL = false>
 __global__ void __launch_bounds__(512, 1) bench(int iters, const float* in, unsigned long long* out, float* sink) {
   uint32_t r[64];
 #pragma unroll
@@ -52,6 +52,15 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, const float* in, unsi
     for (int i = 0; i < 32; ++i) asm volatile("" ::"r"(o[i]));
     const uint64_t hs = f2_add(acc0, acc1);
     tot += f2_lo(hs) + f2_hi(hs) + s0 + s1;
+    if (SERIAL) {
+      // the next half starts only after this one completed (as in the kernel, where the next S
+      // comes from TMEM behind a barrier): no overlap of one half's drain with the next half's fill
+      uint32_t dep = o[31] & 1u;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) dep |= o[i] & 0u;
+      asm volatile("" : "+r"(dep));
+      r[0] ^= dep;
+    }
     // perturb the inputs (packed adds, 32 per half: subtract the "perturb only" line)
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -65,14 +74,14 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, const float* in, unsi
   if (tot == 1.2345f) sink[0] = tot;
 }
 
-template <int MODE, int POLY>
+template <int MODE, int POLY, bool SERIAL = false>
 void run(const char* name, int sms, int warps, const float* in) {
   unsigned long long* d;
   float* sink;
   cudaMalloc(&d, sms * 16 * 8);
   cudaMalloc(&sink, 4);
   const int iters = 4096;
-  bench<MODE, POLY><<<sms, warps * 32>>>(iters, in, d, sink);
+  bench<MODE, POLY, SERIAL><<<sms, warps * 32>>>(iters, in, d, sink);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148 * 16];
   cudaMemcpy(h, d, sms * 16 * 8, cudaMemcpyDeviceToHost);
@@ -103,6 +112,8 @@ int main() {
     run<4, 0>("all MUFU, no row sum", sms, w, in);
     run<5, 0>("all MUFU, no fp16 pack", sms, w, in);
     run<6, 0>("perturb only (baseline)", sms, w, in);
+    run<0, 2, true>("spec body, serialised halves", sms, w, in);
+    run<1, 2, true>("exact body (poly 2/8), serialised", sms, w, in);
   }
   return 0;
 }
