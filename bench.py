@@ -127,6 +127,19 @@ def algorithmic(b, plan_c, hkv_local):
     return flops, kv_bytes, qo_bytes
 
 
+METRIC = "packed prefill TFLOP/s (cfg2 batch step)"
+
+
+def arm_config(b, shard, world):
+    """The workload both arms (this implementation and --impl reference) report as `config`:
+    only what defines the batch, nothing the planner derives (that goes under "plan")."""
+    flops, _, _ = algorithmic(b, None, b.hkv)
+    return {"workload": b.name + " (BASELINE.json configs[1])", "requests": b.n, "tokens": int(b.kv_len.sum()),
+            "hq": b.hq, "hkv": b.hkv, "head_dim": b.d, "capacity": 8192,
+            "l2": "inputs larger than L2 (paged KV 224 MB + Q 448 MB per step > 126 MB)",
+            "parallelism": f"{shard}-sharded x{world}", "algorithmic_tflop": flops / 1e12}
+
+
 class Runner:
     """Owns the device state of one batch and runs steps on one stream (double-buffered plans)."""
 
@@ -379,11 +392,11 @@ def run_reference(args, cfg_name):
         vals.append(f / dt / 1e12)
         secs.append(dt)
     v = sum(vals) / len(vals)
-    line = {"impl": "reference", "metric": "packed prefill TFLOP/s (cfg2 step)", "value": v, "unit": "TFLOP/s",
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * sum(secs) / len(secs), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": b.name, "requests": b.n, "hq": b.hq, "hkv": b.hkv, "head_dim": b.d},
+            "config": arm_config(b, args.shard, args.gpus),
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -459,16 +472,14 @@ def main():
                     "bf16_tflops_sustained", peaks["bf16_tflops"]),
                 "tile_efficiency": pc.valid_cells / max(1, pc.tile_cells)}
 
-    result = {"metric": "packed prefill TFLOP/s (cfg2 batch step)", "value": value, "unit": "TFLOP/s",
+    result = {"metric": METRIC, "value": value, "unit": "TFLOP/s",
               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
               "higher_is_better": True, "scaling": "weak" if args.shard == "group" else "strong",
               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-              "config": {"workload": b.name + " (BASELINE.json configs[1])", "requests": b.n,
-                         "tokens": int(b.kv_len.sum()), "hq": b.hq, "hkv": b.hkv, "head_dim": b.d,
-                         "capacity": 8192, "groups": int(pc.n_groups), "work_items": int(pc.n_prefill_work),
-                         "step": "plan+upload+relayout+prefill(+decode+merge)",
-                         "l2": "inputs larger than L2 (paged KV 224 MB + Q 448 MB per step > 126 MB)",
-                         "parallelism": f"{args.shard}-sharded x{world}", "algorithmic_tflop": flops / 1e12},
+              "config": arm_config(b, args.shard, world),
+              "plan": {"groups": int(pc.n_groups), "work_items": int(pc.n_prefill_work),
+                       "step": "plan+upload+relayout+prefill(+decode+merge)",
+                       "algorithmic_tflop_per_rank": flops / 1e12},
               "roofline": roofline, "clocks": clocks,
               "gpu_launches": runner.launches_per_step * args.steps}
 
