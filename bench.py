@@ -164,6 +164,7 @@ class Runner:
         c = self.pbs[0].plan.c
         self.launches_per_step = 1 + (c.n_prefill_work > 0) + (c.n_decode_work > 0) + (c.n_merges > 0)
         self.kernel_events = []
+        self.step_events = []
 
     def step(self, i, time_kernel=False, t=None, out=None):
         """One batch step on this runner's stream; t / out select another (e.g. double-buffered)
@@ -173,6 +174,9 @@ class Runner:
         q = self.q if t is self.t else t["q"][:, self.hkv_begin * self.r:(self.hkv_begin + self.hkv_count) * self.r]
         out = self.out if out is None else out
         pb = self.pbs[i % 2]
+        if time_kernel:
+            es = torch.cuda.Event(enable_timing=True)
+            es.record(self.stream)
         self.events[i % 2].synchronize()            # host arena of this slot no longer read by H2D
         pb.replan(self.stream)                       # host planner + async upload
         self.events[i % 2].record(self.stream)
@@ -192,6 +196,16 @@ class Runner:
             e2.record(self.stream)
             self.kernel_events.append((e0, e1, e2))
         pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, self.lse, self.stream)
+        if time_kernel:
+            ee = torch.cuda.Event(enable_timing=True)
+            ee.record(self.stream)
+            self.step_events.append((es, ee))
+
+    def step_latency(self):
+        """Per-step device latency (first to last op of the step on the stream): median, p90."""
+        import numpy as np
+        v = np.array([a.elapsed_time(b) for a, b in self.step_events])
+        return {"median_ms": float(np.median(v)), "p90_ms": float(np.percentile(v, 90)), "n": int(v.size)}
 
     def kernel_ms(self):
         pre = [a.elapsed_time(b) for a, b, _ in self.kernel_events]
@@ -209,6 +223,7 @@ def timed_steps(runner, steps, warmup, dist_on):
         dist.barrier()
     torch.cuda.synchronize()
     runner.kernel_events.clear()
+    runner.step_events.clear()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for i in range(steps):
@@ -480,7 +495,7 @@ def main():
               "plan": {"groups": int(pc.n_groups), "work_items": int(pc.n_prefill_work),
                        "step": "plan+upload+relayout+prefill(+decode+merge)",
                        "algorithmic_tflop_per_rank": flops / 1e12},
-              "roofline": roofline, "clocks": clocks,
+              "roofline": roofline, "clocks": clocks, "step_latency": runner.step_latency(),
               "gpu_launches": runner.launches_per_step * args.steps}
 
     if dist_on and args.shard == "heads":
@@ -521,7 +536,8 @@ def main():
                             "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
                             "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9,
                             "work_items": int(rd.pbs[0].plan.c.n_decode_work),
-                            "partial_slots": int(rd.pbs[0].plan.c.n_partial_slots)}
+                            "partial_slots": int(rd.pbs[0].plan.c.n_partial_slots),
+                            "step_latency": rd.step_latency()}
         result["decode"]["gpu_launches"] = rd.launches_per_step * max(3, args.steps)
         del rd
 
