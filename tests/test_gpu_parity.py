@@ -45,6 +45,22 @@ def test_relayout_bitwise(C, delta):
         assert (got[:, ~valid] == 0).all()           # headroom zero-filled
 
 
+@pytest.mark.parametrize("delta", [0, 5])
+def test_relayout_many_copies(delta):
+    """~2k copy entries: the relayout's 32-ary copy-entry search takes several rounds, and buffer
+    cells sit on every kind of entry boundary (prefix / suffix / headroom / group base)."""
+    b = W.random_batch(9, n=2000, max_len=24, hq=4, hkv=2, d=64, n_prefix=3)
+    t = W.make_tensors(b, device="cuda")
+    _, _, pb = H.run_batch(b, t, C=256, delta=delta)
+    op = OP.plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, 256, headroom=delta)
+    assert len(op.copies) > 1024
+    want, valid = OL.expected_buffers(op.copies, t["k_paged"].cpu(), t["block_table"].cpu(), b.n, b.page_size,
+                                      op.buffer_tokens)
+    got = pb.k_buf.cpu().view(torch.int16).numpy()
+    assert np.array_equal(got[:, valid], want[:, valid])
+    assert (got[:, ~valid] == 0).all()
+
+
 def test_relayout_head_slice():
     b = W.random_batch(2, n=6, max_len=300, hq=8, hkv=4, d=64)
     t = W.make_tensors(b, device="cuda")
