@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, const float* in, unsi
   float tot = 0.f;
   __syncwarp();
   const long long t0 = clock64();
+#pragma unroll 1
   for (int it = 0; it < iters; ++it) {
     uint32_t o[32];
     uint64_t acc0 = 0, acc1 = 0;
