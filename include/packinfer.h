@@ -214,7 +214,11 @@ PI_API pi_status packinfer_plan_upload(const pi_plan* plan, void* dev_arena, siz
 /* ------------------------------------------------------------------------------------------
  * Contiguous memory consolidation (Alg. 1 Copy lines P:244/P:250; §3.2):
  * gather every copy-plan entry from the paged cache into k_buf/v_buf for KV heads
- * [hkv_begin, hkv_begin + hkv_count).  Bitwise copy; headroom cells are not written.
+ * [hkv_begin, hkv_begin + hkv_count).  Bitwise copy (V of bf16 caches as fp16); headroom cells
+ * are zero-filled.  The cells written are those of the device plan's copy list (copy_prefix
+ * [n_copies] of them; a batch plan covers all buffer_tokens).  A caller may pass a device plan
+ * whose copies / copy_prefix are a subsequence of the batch's (group sharding of one batch,
+ * SURVEY 8(e)): destinations stay in batch coordinates, k_buf/v_buf keep buffer_tokens rows.
  * ---------------------------------------------------------------------------------------- */
 PI_API pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void* k_paged,
                                 const void* v_paged, const int32_t* block_table,

@@ -24,7 +24,7 @@ struct RelayoutParams {
   const pi_copy* copies;
   const int64_t* ext_prefix;  // [n_copies + 1] cumsum of buffer cells per copy (len + headroom)
   int32_t n_copies;
-  int64_t total;              // == buffer_tokens
+  int64_t total;              // buffer_tokens: grid size (an upper bound of the cells to write)
   int32_t n_requests;
   const uint8_t* kp;
   const uint8_t* vp;
@@ -81,11 +81,14 @@ __device__ __forceinline__ int find_copy(const int64_t* __restrict__ ext_prefix,
 __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
   const int64_t g0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RL_TPW;
   const int lane = threadIdx.x & 31;
-  if (g0 >= p.total) return;
+  // cells to write = the copy list's own cell count (== buffer_tokens for a batch plan; a rank's
+  // share under group sharding, shard.RankPlan, is smaller: the grid covers buffer_tokens)
+  const int64_t total = __ldg(&p.ext_prefix[p.n_copies]);
+  if (g0 >= total) return;
   int c = find_copy(p.ext_prefix, p.n_copies, g0, lane);
   int64_t next = c + 1 < p.n_copies ? __ldg(&p.ext_prefix[c + 1]) : INT64_MAX;
   const int64_t row_bytes = (int64_t)p.head_chunks * 16;
-  const int64_t g_end = min(g0 + RL_TPW, p.total);
+  const int64_t g_end = min(g0 + RL_TPW, total);
   for (int64_t g = g0; g < g_end; ++g) {
     while (g >= next) {   // next copy entry (copies are long: rarely taken)
       ++c;

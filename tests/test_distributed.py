@@ -57,6 +57,24 @@ def _worker(rank, world, port, q):
         heads = [None] * world
         dist.all_gather_object(heads, list(range(hb, hb + hc)))
         res["heads"] = sorted(h for hs in heads for h in hs)
+        # group sharding of one batch: shard.combine assembles slots / rows owned by one rank each
+        g2 = torch.Generator().manual_seed(11)
+        po_full = torch.randn((6, 4, 8), generator=g2)
+        pl_full = torch.randn((6, 4), generator=g2)
+        out_full = torch.randn((5, 4, 8), generator=g2)
+        po, pl, o, l = torch.empty(6, 4, 8), torch.empty(6, 4), torch.empty(5, 4, 8), torch.empty(4, 5)
+        shard.init_partials(po, pl, o, l)
+        for sl in range(6):
+            if sl % world == rank:
+                po[sl], pl[sl] = po_full[sl], pl_full[sl]
+        for row in range(5):
+            if row % world == rank:
+                o[row] = out_full[row]
+                l[:, row] = float(row)
+        shard.combine(po, pl, o, l)
+        res["combine_equal"] = bool(torch.equal(po, po_full) and torch.equal(pl, pl_full)
+                                    and torch.equal(o, out_full)
+                                    and torch.equal(l, torch.arange(5.0).expand(4, 5)))
         # bench.py's max-over-ranks step time
         t = torch.tensor([1.0 + rank])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -86,6 +104,7 @@ def test_two_rank_gloo():
             assert res[name + "_balance"], name
         assert res["heads"] == list(range(8))
         assert res["gather_equal"]
+        assert res["combine_equal"]
         assert res["tmax"] == 2.0
 
 
@@ -108,3 +127,32 @@ def test_group_shard_lpt_bound():
             loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(world)]
             # LPT guarantee: max load <= mean + max item
             assert max(loads) <= sum(costs) / world + max(costs)
+
+
+def test_rank_plan_partitions_decode_batch():
+    """Group sharding of one decode batch (shard.RankPlan host logic): every decode work item and
+    every copy entry belongs to exactly one rank, the ranks' buffer cells add up to the batch's, and
+    each rank's copy subsequence keeps the batch cell prefix's per-entry extents."""
+    import numpy as np
+    from synth import workloads as W
+    from paper_2602_06072_b200 import packinfer as pk, shard
+    b = W.random_batch(31, n=24, max_len=1500, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    cfg = pk.default_config(capacity=256, decode_chunk=256, gqa_ratio=4)
+    hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, cfg)
+    cg = shard.copy_groups(hp)
+    bases = np.asarray(hp.groups["base"])
+    caps = np.asarray(hp.groups["cap"])
+    dst = np.asarray(hp.copies["dst"])
+    assert ((dst >= bases[cg]) & (dst < bases[cg] + caps[cg])).all()
+    prefix = np.asarray(hp.copy_prefix)
+    assert prefix[-1] == hp.c.buffer_tokens
+    for world in (1, 2, 3, 5):
+        owner = np.asarray(shard.group_shard(shard.group_costs(hp), world))
+        w_rank = owner[np.asarray(hp.decode_work["group"])]
+        c_rank = owner[cg]
+        assert np.bincount(w_rank, minlength=world).sum() == hp.c.n_decode_work
+        cells = [int((prefix[1:] - prefix[:-1])[c_rank == r].sum()) for r in range(world)]
+        assert sum(cells) == hp.c.buffer_tokens
+        # LPT balance: no rank above the mean by more than the largest group
+        load = np.bincount(owner, weights=shard.group_costs(hp), minlength=world)
+        assert load.max() - load.mean() <= max(shard.group_costs(hp))

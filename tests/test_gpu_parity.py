@@ -303,3 +303,47 @@ def test_decode_loop_append():
                               b.q_len, b.page_size)
         H.compare(out, lse, ro, rl)
     assert regroups >= 1                              # the headroom (4) ran out within 10 steps
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_decode_group_sharding_one_batch(world):
+    """Group sharding of ONE decode batch (shard.RankPlan), the ranks simulated one after the other
+    on cuda:0: each consolidates and attends only its groups; the SUM/MAX combine of shard.combine
+    (done here with the same torch reductions) + the batch plan's merge equal the oracle, and the
+    union of the ranks' buffers equals the single-rank consolidation bitwise."""
+    from paper_2602_06072_b200 import packinfer as pk, shard
+    b = W.random_batch(31, n=24, max_len=1500, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    assert (b.q_len == 1).all()
+    t = W.make_tensors(b, device="cuda")
+    r = b.hq // b.hkv
+    pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, t["q"].dtype, "cuda",
+                        capacity=256, decode_chunk=256)
+    owner = shard.group_shard(shard.group_costs(pb.plan), world)
+    assert len(set(owner)) == world
+    po_all, pl_all, out_all, lse_all, kbuf = [], [], [], [], []
+    for rank in range(world):
+        rp = shard.RankPlan(pb, owner, rank)
+        kb = torch.zeros_like(pb.k_buf)
+        vb = torch.zeros_like(pb.v_buf)
+        pk.packinfer_relayout_kv(rp.dp, t["k_paged"], t["v_paged"], t["block_table"], kb, vb, 0, b.hkv)
+        po, pl = torch.empty_like(pb.partial_o), torch.empty_like(pb.partial_lse)
+        out = torch.empty((b.total_q, b.hq, b.d), dtype=t["q"].dtype, device="cuda")
+        lse = torch.empty((b.hq, b.total_q), dtype=torch.float32, device="cuda")
+        shard.init_partials(po, pl, out, lse)
+        pk.packinfer_attention_decode(rp.dp, t["q"], kb, vb, out, lse, po, pl, r)
+        po_all.append(po); pl_all.append(pl); out_all.append(out); lse_all.append(lse); kbuf.append(kb)
+    torch.cuda.synchronize()
+    # the all-reduces of shard.combine
+    po = torch.stack(po_all).sum(0)
+    pl = torch.stack(pl_all).amax(0)
+    out = torch.stack(out_all).float().sum(0).to(t["q"].dtype)
+    lse = torch.stack(lse_all).amax(0)
+    pk.packinfer_merge(pb.dp, po, pl, out, lse)
+    torch.cuda.synchronize()
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out, lse, ro, rl)
+    # consolidation: every cell written by exactly one rank, equal to the batch relayout
+    pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf, pb.v_buf, 0, b.hkv)
+    torch.cuda.synchronize()
+    union = torch.stack([k.view(torch.int16) for k in kbuf]).sum(0, dtype=torch.int64)
+    assert torch.equal(union, pb.k_buf.view(torch.int16).to(torch.int64))
