@@ -440,11 +440,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: PI_BENCH_ONE_GPU=1 puts every rank on cuda:0 with gloo (exercises the N > 1 code
+    # path on a one-GPU box; never used for a reported number)
+    one_gpu = os.environ.get("PI_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist_on = world > 1
     if dist_on:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peak_src = load_peaks()
     dev = torch.device("cuda", local)
 
