@@ -293,6 +293,59 @@ def e2e_steps(b, runner, steps):
     return s.elapsed_time(e) / steps, h2d, d2h
 
 
+def decode_group_sharded(dev, rank, world, args, peaks):
+    """N > 1 only: ONE configs[2] decode batch (the same on every rank) group-sharded across the
+    ranks (shard.RankPlan, SURVEY 8(e) optional group sharding): each rank consolidates and attends
+    only its groups; split rows are completed by shard.combine (SUM / MAX all-reduce over NCCL) and
+    the batch merge.  Step = relayout (own groups) + decode attention (own items) + combine + merge,
+    timed with CUDA events, max over ranks (strong scaling of one batch)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_06072_b200 import packinfer as pk, shard
+    bd = make_workload("cfg3", 0)
+    r = bd.hq // bd.hkv
+    t = W_tensors(bd, dev)
+    pb = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, bd.hkv, r, bd.d, t["q"].dtype, dev)
+    owner = shard.group_shard(shard.group_costs(pb.plan), world)
+    rp = shard.RankPlan(pb, owner, rank)
+    out = torch.empty((bd.total_q, bd.hq, bd.d), dtype=t["q"].dtype, device=dev)
+    st = torch.cuda.current_stream()
+
+    def once():
+        pk.packinfer_relayout_kv(rp.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf, pb.v_buf, 0,
+                                 bd.hkv, st)
+        shard.init_partials(pb.partial_o, pb.partial_lse, out)
+        pk.packinfer_attention_decode(rp.dp, t["q"], pb.k_buf, pb.v_buf, out, None, pb.partial_o,
+                                      pb.partial_lse, r, 0.0, st)
+        shard.combine(pb.partial_o, pb.partial_lse, out)
+        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, None, st)
+
+    for _ in range(args.warmup):
+        once()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(3, args.steps)
+    e0.record(st)
+    for _ in range(n):
+        once()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / n], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    kv_bytes = 2 * int(pb.plan.c.copy_tokens) * bd.hkv * bd.d * 2
+    return {"workload": bd.name + " (BASELINE.json configs[2]), one batch over all ranks",
+            "ms_per_step": float(ms[0]), "step_gbs": kv_bytes / (float(ms[0]) * 1e-3) / 1e9,
+            "rank_cells": rp.cells, "rank_work_items": rp.n_work, "groups": int(pb.plan.c.n_groups),
+            "scaling": "strong", "note": "relayout + decode attention of this rank's groups, SUM/MAX "
+                                         "all-reduce of partials and direct rows, merge"}
+
+
+def W_tensors(b, dev):
+    from synth import workloads as W
+    return W.make_tensors(b, device=dev, seed=b.seed)
+
+
 def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
     """BASELINE.json configs[4]: Llama-3-70B-shaped mixed batch (2 x 128k-token prefills split
     across groups + 30 short prefills + 224 decodes up to 32k), ONE fused attention launch over
@@ -548,6 +601,9 @@ def main():
                             "step_latency": rd.step_latency()}
         result["decode"]["gpu_launches"] = rd.launches_per_step * max(3, args.steps)
         del rd
+
+    if dist_on and not args.no_decode:
+        result["decode_group_sharded"] = decode_group_sharded(dev, rank, world, args, peaks)
 
     if not args.no_decode and not args.no_loop:
         # Decode loop (NEXT-1): consolidate once with headroom delta = 32
