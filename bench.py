@@ -547,6 +547,15 @@ def main():
                 "peak_source": peak_src + " bf16 burst", "frac_of_sustained": achieved / peaks.get(
                     "bf16_tflops_sustained", peaks["bf16_tflops"]),
                 "tile_efficiency": pc.valid_cells / max(1, pc.tile_cells)}
+    # The softmax's exponentials have their own ceiling: one exp2 per visible
+    # (query, key) pair and query head, 16 per clock per SM on MUFU (measured,
+    # profiles/r01d/mufu_bench.txt); the kernel moves 2 of 8 pairs to the FMA pipe.
+    n_exp = flops / (4 * b.d)                                   # = Hq_local * visible pairs
+    sm_hz = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    roofline["exp_ceiling"] = {"exps": n_exp, "mufu_only_ms_at_max_clock": n_exp / (16 * nsm * sm_hz) * 1e3,
+                               "tensor_only_ms_at_max_clock": flops / (8192 * nsm * sm_hz) * 1e3,
+                               "note": "dense bf16 tcgen05 = 8192 FLOP/clk/SM; MUFU ex2 = 16/clk/SM"}
 
     result = {"metric": METRIC, "value": value, "unit": "TFLOP/s",
               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
