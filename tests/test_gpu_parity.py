@@ -99,6 +99,24 @@ def test_random_mixed_bf16(seed, d, out_f32):
     H.compare(out, lse, ro, rl)
 
 
+@pytest.mark.parametrize("seed", range(200, 240))
+def test_random_sweep_small(seed):
+    """Forty more seeded mixed batches (prefill, suffix prefill over shared prefixes, decode, splits
+    at small C, headroom, both head dims and GQA ratios), fused launch, element-wise vs the oracle."""
+    rng = np.random.default_rng(seed)
+    hkv = int(rng.choice([1, 2, 3]))
+    r = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    b = W.random_batch(seed, n=int(rng.integers(1, 10)), max_len=int(rng.integers(2, 600)), hq=hkv * r, hkv=hkv,
+                       d=d, n_prefix=int(rng.integers(0, 3)), decode_frac=float(rng.choice([0.0, 0.3, 1.0])),
+                       page_size=int(rng.choice([128, 256])))
+    C = int(rng.choice([8192, 384, 130]))
+    t = W.make_tensors(b, device="cuda")
+    out, lse, _ = H.run_batch(b, t, C=C, delta=int(rng.integers(0, 5)), decode_chunk=128 * int(rng.integers(1, 3)))
+    ro, rl = H.oracle_full(b, t)
+    H.compare(out, lse, ro, rl)
+
+
 def test_peaky_queries():
     """q x 4 stresses the max-subtraction / lazy rescale path."""
     b = W.random_batch(77, n=8, max_len=800, hq=8, hkv=2, d=128)
