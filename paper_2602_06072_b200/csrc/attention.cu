@@ -10,18 +10,23 @@
 // heads of the same GQA group — which share every K/V tile and every mask, so one TMA stream feeds
 // two tensor-core pipelines.  Decode units carry one tile (its rows already span the GQA group).
 //
-// Per CTA (one per SM, 384 threads, warp-specialised):
+// Per CTA (one per SM, 384 threads, warp-specialised, setmaxnreg 56 / 216):
 //   warp 0    TMA producer: K/V tiles (128 keys x d, SWIZZLE_128B) into a 2-stage ring
-//   warp 1    TMEM allocator + single-thread tcgen05.mma issuer, FA4-style ping-pong:
-//               S_X = Q_X K^T -> TMEM S_X     (SS, M=128 N=128 K=d)
-//               O_X += P_X V  -> TMEM O_X     (TS: P_X read from TMEM where it overwrote S_X)
-//             issue order  S_A0 S_B0 | PV_A0 S_A1 | PV_B0 S_B1 | PV_A1 S_A2 | ...
-//   warp 2    Q gather for both tiles through the plan's row table (cp.async, 128 B swizzle)
+//   warp 1    TMEM allocator + converged tcgen05.mma issuer (elect.sync), FA4-style ping-pong:
+//               S_X = Q_X K^T -> TMEM S_X     (SS, M=128 N=128 K=d, one chain)
+//               O_X += P_X V  -> TMEM O_X     (TS: P_X read from TMEM where it overwrote S_X,
+//                                              in two 64-key halves as the softmax releases them)
+//             per K tile j: PV_A(j) half 0 | half 1, S_A(j+1) | PV_B(j) half 0 | half 1, S_B(j+1)
+//             (single-tile decode units: S regions alternate per tile, the two warpgroups split
+//             the keys of every tile into O_0 / O_1, LSE-merged in the epilogue)
+//   warp 2    Q gather for both tiles through the plan's row table (TMA tile::gather4)
 //   warp 3    fp32 operands only: stages V^T (K-major) for kind::tf32
 //   warps 4-7 softmax / correction / epilogue of tile A; warps 8-11 of tile B.  Thread i owns
-//             row i (= TMEM lane i), so row max / sum need no shuffles.  Two TMEM passes per tile
-//             (max, then exp2 + pack + store P) keep register pressure low; the O rescale is lazy
-//             (only when the running max grows by > 2^8) and happens in TMEM.
+//             row i (= TMEM lane i), so row max / sum need no shuffles.  One streaming pass per
+//             64-column half (each S element read from TMEM once); once the running max is set an
+//             unmasked half is exponentiated speculatively against it and certified by its sum;
+//             the O rescale is lazy (only when the running max grows by > 2^8) and happens in TMEM.
+//             exp2: MUFU for 6 of every 8 pairs, a minimax cubic on the FMA pipe for the rest.
 // bf16 operands run kind::f16, fp32 operands kind::tf32; accumulation fp32 (reading R13).
 #include <cuda.h>
 #include <cuda_runtime.h>
