@@ -128,8 +128,10 @@ struct AttnCfg {
 };
 
 // S/P regions b = 0/1 complete per half-tile: SF[b][h] (S columns 64h..64h+63 landed), PHALF[b]
-// (P for keys 0..63 written), PFULL[b] (P for keys 64..127 written).  PVH[X]: the first half of
-// P.V into O slot X landed (only waited on for a rare mid-tile rescale).
+// (P for keys 0..63 written), PFULL[b] (P for keys 64..127 written).  PVH[X] (pair units): the
+// first half of P.V into O slot X landed.  Committed every tile, waited only by a rare mid-tile
+// rescale (compute-sanitizer synccheck reports its unwaited phases; the waiter computes the parity
+// of the phase it needs, which cannot be overtaken: PV(j+1) needs this warpgroup's P(j+1)).
 enum BarId {
   B_QFULL = 0, B_QFREE, B_KFULL0, B_KFULL1, B_KFREE0, B_KFREE1, B_VFULL0, B_VFULL1, B_VFREE0, B_VFREE1,
   B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
@@ -418,7 +420,6 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             // split-K inside the CTA: keys 0..63 of every tile -> O_0 (softmax warpgroup A),
             // keys 64..127 -> O_1 (warpgroup B); the epilogue merges the two (LSE)
             issue_pv(0, b ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
-            commit(B_PVH0);
             mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
             tc_fence_after();
             issue_pv(1, (b ? C::TM_S1 : C::TM_S0) + C::P1_SINGLE, tt, j == 0, 1);
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         cnt1[0] += (n + 1) >> 1;
         cnt1[1] += n >> 1;
       }
-      if (u.has_b || X == 0) pvh += n;   // PVH1 completes for pair units only
+      if (u.has_b) pvh += n;   // PVH completes for pair units only
       t += n;
       ++ix;
     }
