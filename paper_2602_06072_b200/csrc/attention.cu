@@ -39,6 +39,9 @@
 #include "packinfer.h"
 #include "sm100.cuh"
 
+#ifndef PI_POLY_SAT
+#define PI_POLY_SAT 1
+#endif
 #ifndef PI_POLY_PAIRS
 #define PI_POLY_PAIRS 2   // of every 8 score pairs, this many take exp2 on the FMA pipe (A/B: scripts/ab_poly.sh)
 #endif
@@ -606,12 +609,20 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           // (use_poly: PI_POLY_PAIRS of 8 pairs on the FMA pipe; clamp: x unbounded, see ex2_poly2)
           auto exp_body = [&](auto use_poly, auto clamp, uint64_t SL2, uint64_t NM, uint64_t& acc0,
                               uint64_t& acc1) {
+#if PI_POLY_SAT
+            // poly pairs take the argument saturated (ex2_poly_sat): A = scale / 252, B = (125 - m) / 252
+            const float PA = f2_lo(SL2) * (1.0f / 252.0f), PB = (f2_lo(NM) + 125.0f) * (1.0f / 252.0f);
+#endif
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const uint64_t x = f2_fma(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), SL2, NM);
               uint64_t e;
               if (decltype(use_poly)::value && (i & 7) >= 8 - PI_POLY_PAIRS)
+#if PI_POLY_SAT
+                e = ex2_poly_sat(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), PA, PB);
+#else
                 e = ex2_poly2<decltype(clamp)::value>(x);
+#endif
               else
                 e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
               if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);

@@ -288,5 +288,27 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
   return f2(__uint_as_float(lo), __uint_as_float(hi));
 }
 
+// exp2 of x = s * scale - m for a pair of raw scores on the FMA pipe, clamp-free: the argument is
+// formed saturated, x' = sat(s * A + B) in [0, 1] with A = scale / 252, B = (125 - m) / 252
+// (scalar FFMA.SAT, 1 issue cycle each), so y = 252 x' - 125 = clamp(x, -125, 127) needs no
+// FMNMX; 2^y = 2^round(y) * p(y - round(y)) with the same minimax cubic as ex2_poly2.
+__device__ __forceinline__ uint64_t ex2_poly_sat(float s_lo, float s_hi, float A, float B) {
+  float xl, xh;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(xl) : "f"(s_lo), "f"(A), "f"(B));
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(xh) : "f"(s_hi), "f"(A), "f"(B));
+  const float MAGIC = 12582912.0f;
+  const uint64_t xs = f2(xl, xh);
+  const uint64_t t = f2_fma(xs, f2(252.0f, 252.0f), f2(MAGIC - 125.0f, MAGIC - 125.0f));   // MAGIC + round(y)
+  const uint64_t nn = f2_fma(t, f2(-1.0f, -1.0f), f2(MAGIC - 125.0f, MAGIC - 125.0f));   // -125 - round(y)
+  const uint64_t f = f2_fma(xs, f2(252.0f, 252.0f), nn);                                 // y - round(y)
+  uint64_t p = f2_fma(f, f2(0.0551710967f, 0.0551710967f), f2(0.2426099964f, 0.2426099964f));
+  p = f2_fma(p, f, f2(0.6932609731f, 0.6932609731f));
+  p = f2_fma(p, f, f2(0.9999281437f, 0.9999281437f));
+  const uint32_t tl = __float_as_uint(f2_lo(t)), th = __float_as_uint(f2_hi(t));
+  const uint32_t lo = __float_as_uint(f2_lo(p)) + (tl << 23);
+  const uint32_t hi = __float_as_uint(f2_hi(p)) + (th << 23);
+  return f2(__uint_as_float(lo), __uint_as_float(hi));
+}
+
 }  // namespace sm100
 }  // namespace pi
