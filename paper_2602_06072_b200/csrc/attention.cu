@@ -80,13 +80,18 @@ struct AttnParams {
 
 // Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
 constexpr int TRACE_TILES = 64;
+// Compiled in only with -DPI_TRACE=1 (scripts/trace_*.py build such a variant): the hot loops of
+// the production build carry no trace checks.
+#ifndef PI_TRACE
+#define PI_TRACE 0
+#endif
 __device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int ev) {
-  if (p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
+  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
     p.trace[tile * 24 + ev] = clock64();
 }
 // Per-unit events: trace[1024 + unit * 8 + ev], first 64 units of CTA 0.
 __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
-  if (p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[64 * 24 + unit * 8 + ev] = clock64();
+  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[64 * 24 + unit * 8 + ev] = clock64();
 }
 
 template <int D, bool F32>
@@ -724,8 +729,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               ps[3] = f2_hi(acc1);
               }
               if (row_id == 0 && h == 0) trace_ev(p, t + j, 22 + X);
-              if (p.trace != nullptr) spec_bits |= (spec_done ? 1u : 0u) << h;
-              if (row_id == 0 && h == 1 && p.trace != nullptr && blockIdx.x == 0 && t + j < (uint32_t)TRACE_TILES)
+              if (PI_TRACE && p.trace != nullptr) spec_bits |= (spec_done ? 1u : 0u) << h;
+              if (PI_TRACE && row_id == 0 && h == 1 && p.trace != nullptr && blockIdx.x == 0 &&
+                  t + j < (uint32_t)TRACE_TILES)
                 p.trace[(t + j) * 24 + 17 + 2 * X] = spec_bits;
               if constexpr (!F32) {
                 // pair units: P_h at 32h (over S columns already read); single units: warpgroup

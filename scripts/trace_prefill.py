@@ -1,6 +1,14 @@
 """CTA-0 timeline of the packed attention kernel on the cfg2 prefill batch (debug hook)."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# the trace hooks are compiled in only with -DPI_TRACE=1: build that variant and load it
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_LIB = os.path.join(_ROOT, "variants", "libpi_trace.so")
+if "PACKINFER_LIB" not in os.environ:
+    from paper_2602_06072_b200 import build as _B
+    os.makedirs(os.path.dirname(_LIB), exist_ok=True)
+    _B.build(True, False, _LIB, ("PI_TRACE=1",))
+    os.environ["PACKINFER_LIB"] = _LIB
 import numpy as np, torch
 from synth import workloads as W
 from paper_2602_06072_b200 import packinfer as pk
