@@ -100,9 +100,10 @@ def lib():
     """Loads libpackinfer.so (raises if it is missing — there is no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise PackInferError(PI_EUNSUP, "load", f"{_LIB_PATH} not built (run __graft_entry__.build())")
-        L = C.CDLL(_LIB_PATH)
+        path = os.environ.get("PACKINFER_LIB") or _LIB_PATH   # read at first load (A/B variants)
+        if not os.path.exists(path):
+            raise PackInferError(PI_EUNSUP, "load", f"{path} not built (run __graft_entry__.build())")
+        L = C.CDLL(path)
         vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
         L.packinfer_strerror.restype = C.c_char_p
         L.packinfer_strerror.argtypes = [C.c_int]
