@@ -31,9 +31,8 @@
  *                 prefix p's tokens [0, prefix_len[p]).
  *   k/v_buf       [hkv_count, buffer_tokens, head_dim]  group-contiguous buffers B_g laid end
  *                 to end (base_g = sum of earlier group capacities)       (Alg. 1 Part 2).
- *                 Internal workspace: for PI_BF16 caches k_buf holds bf16 (bitwise copies) and
- *                 v_buf holds fp16 (exact conversion for |v| < 65504, saturated beyond), which
- *                 lets the kernels multiply an fp16 P; for PI_FP32 both are fp32.
+ *                 Element type = the cache's (bf16 or fp32): every cell is a bitwise copy of
+ *                 the paged cache (no conversion, the full bf16 range is preserved).
  *   partial_o     fp32 [n_partial_slots, hq_count, head_dim]; partial_lse fp32
  *                 [n_partial_slots, hq_count] — partial results of split rows (reading R10).
  */
@@ -214,7 +213,7 @@ PI_API pi_status packinfer_plan_upload(const pi_plan* plan, void* dev_arena, siz
 /* ------------------------------------------------------------------------------------------
  * Contiguous memory consolidation (Alg. 1 Copy lines P:244/P:250; §3.2):
  * gather every copy-plan entry from the paged cache into k_buf/v_buf for KV heads
- * [hkv_begin, hkv_begin + hkv_count).  Bitwise copy (V of bf16 caches as fp16); headroom cells
+ * [hkv_begin, hkv_begin + hkv_count).  Bitwise copy of K and V; headroom cells
  * are zero-filled.  The cells written are those of the device plan's copy list (copy_prefix
  * [n_copies] of them; a batch plan covers all buffer_tokens).  A caller may pass a device plan
  * whose copies / copy_prefix are a subsequence of the batch's (group sharding of one batch,
@@ -239,8 +238,8 @@ PI_API pi_status packinfer_append_kv(const pi_device_plan* dp, const void* k_new
  * Packed attention ("union of valid query-key regions"; P:172 one launch for every
  * group): ONE persistent launch over all prefill (resp. decode) work items x local heads.
  * S = scale * Q K^T and O += P V run on tcgen05 (TMEM accumulators, TMA-fed K/V), softmax is
- * online with fp32 statistics; bf16 Q/K, fp32 accumulation, P rounded to fp16 against the fp16
- * V of the group buffers (reading R13; PI_FP32 uses kind::tf32).  q/out: local heads [0, hkv_count*gqa_ratio) of each token
+ * online with fp32 statistics; bf16 Q/K/V, fp32 accumulation, P rounded to bf16 for P.V
+ * (reading R13; PI_FP32 uses kind::tf32).  q/out: local heads [0, hkv_count*gqa_ratio) of each token
  * (strides in elements); rows with a single result write out/lse directly, split rows write
  * (o, lse) to partial slots for packinfer_merge.  head_dim in {64, 128}.
  * lse may be NULL.  softmax_scale <= 0 selects 1/sqrt(head_dim).

@@ -39,6 +39,9 @@
 #include "packinfer.h"
 #include "sm100.cuh"
 
+#ifndef PI_P_F16
+#define PI_P_F16 0   // experiment: P packed as fp16 against bf16 V (idesc a_fmt = f16, b_fmt = bf16)
+#endif
 #ifndef PI_POLY_SAT
 #define PI_POLY_SAT 1
 #endif
@@ -110,8 +113,8 @@ struct AttnCfg {
   static constexpr int OFF_K = 2 * TILE_BYTES;
   static constexpr int OFF_V = OFF_K + NS * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
-  static constexpr int OFF_XCH = OFF_BAR + 256;       // single units: (m, l) of both warpgroups
-  static constexpr int SMEM = OFF_XCH + 2 * 128 * 8 + 1024;   // + alignment slack
+  static constexpr int OFF_XCH = OFF_BAR + 256;       // single units: (m, l, l_rounded) of both warpgroups
+  static constexpr int SMEM = OFF_XCH + 2 * 128 * 16 + 1024;  // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
   // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
   static constexpr uint32_t P1_SINGLE = F32 ? 64u : 96u;
@@ -120,9 +123,9 @@ struct AttnCfg {
   static constexpr uint32_t IDESC_QK128 = idesc_make(FMT, 128, 128, 0, 0);  // pair units: one N=128 S
   // bf16: V is the MN-major B operand straight from TMA.  fp32 (kind::tf32): MN-major tf32 needs
   // the 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
-  // P is stored as fp16 (10-bit mantissa: 8x smaller rounding than bf16; P <= 2^8 by the lazy
-  // rescale) and the relayout keeps V as fp16 in the group buffers: P.V is kind::f16 with f16 x f16.
-  static constexpr uint32_t IDESC_PV = F32 ? idesc_make(FMT, 128, D, 0, 0) : idesc_make2(0, 0, 128, D, 0, 1);
+  // P is rounded to bf16 (P <= 2^8 by the lazy rescale) and V is the bitwise bf16 copy in the group
+  // buffers: P.V is kind::f16 with bf16 x bf16, V the MN-major B operand (reading R13).
+  static constexpr uint32_t IDESC_PV = F32 ? idesc_make(FMT, 128, D, 0, 0) : idesc_make2(PI_P_F16 ? 0 : 1, 1, 128, D, 0, 1);
   static constexpr int VT_ATOM_BYTES = D * 128;       // fp32 V^T: D rows x 32 keys
   static constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
   // warps 0..ROLE-1: TMA producer, MMA issuer, Q gather (+ V^T staging for fp32); then two softmax
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       const bool warp_any = wq * 32 < wk.row_count;
       pi_row row = {0, 0, 0, 0};
       if (valid) row = p.rows[wk.row_begin + row_id];
-      float m_ref = NEG_INF, l = 0.f;
+      float m_ref = NEG_INF, l = 0.f, lr = 0.f;   // running max (log2 units), exact / rounded-P sums
       uint32_t j = 0;
       for (int s = 0; s < wk.span_count; ++s) {
         const pi_span sp = p.spans[wk.span_begin + s];
@@ -585,7 +588,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             c_hi = hi_k - k0;
           }
           const bool full = (c_lo == 0 && c_hi == 128);
-          float ps[4] = {0.f, 0.f, 0.f, 0.f};
+          float ps[4] = {0.f, 0.f, 0.f, 0.f};   // exact row sum of this tile's P (LSE)
+          float rs[4] = {0.f, 0.f, 0.f, 0.f};   // row sum of the bf16-rounded P (O normalisation)
           // Streaming single pass over two 64-column halves, each released to the tensor core as
           // soon as it is written: each S element is read from TMEM once; the running max is lazy
           // (updated only when it grows by > 2^8).  A jump in the first half rescales O before any
@@ -610,10 +614,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           }
           if (row_id == 0) trace_ev(p, t + j, 20 + X);
           uint32_t spec_bits = 0;
-          // exp2 of the 64 scores in r, packed in place (fp16 pairs into r[0..31]; fp32 stays put)
+          // exp2 of the 64 scores in r, packed in place (bf16 pairs into r[0..31]; fp32 stays put)
           // (use_poly: PI_POLY_PAIRS of 8 pairs on the FMA pipe; clamp: x unbounded, see ex2_poly2)
-          auto exp_body = [&](auto use_poly, auto clamp, uint64_t SL2, uint64_t NM, uint64_t& acc0,
-                              uint64_t& acc1) {
+          // Two row sums: the exact fp32 sum of P (acc0/acc1, FADD2) gives the LSE and certifies the
+          // speculative half; the sum of the ROUNDED bf16 P that P.V multiplies (racc, FHADD.BF16:
+          // fp32 += bf16 half, no unpacking) normalises O, so O / l is a convex combination of V rows
+          // with the kernel's own weights (reading R13).
+          auto exp_body = [&](auto use_poly, auto clamp, uint64_t SL2, uint64_t NM, uint64_t& acc0, uint64_t& acc1,
+                              float (&racc)[4]) {
 #if PI_POLY_SAT
             // poly pairs take the argument saturated (ex2_poly_sat): A = scale / 252, B = (125 - m) / 252
             const float PA = f2_lo(SL2) * (1.0f / 252.0f), PB = (f2_lo(NM) + 125.0f) * (1.0f / 252.0f);
@@ -632,7 +640,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                 e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
               if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
               if constexpr (!F32) {
-                r[i] = pack_f16(f2_lo(e), f2_hi(e));      // in place: i <= 2i
+                r[i] = pack_bf16(f2_lo(e), f2_hi(e));     // in place: i <= 2i
+                add_bf16x2(racc[2 * (i & 1)], racc[2 * (i & 1) + 1], r[i]);
               } else {
                 r[2 * i] = __float_as_uint(f2_lo(e));
                 r[2 * i + 1] = __float_as_uint(f2_hi(e));
@@ -655,7 +664,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                 // rows of an earlier unit (their results are discarded) and must not steer it
                 if (__all_sync(0xffffffffu, !valid || (full && m_ref != NEG_INF))) {
                   uint64_t a0 = 0, a1 = 0;
-                  exp_body(std::true_type{}, std::true_type{}, f2(sl2, sl2), f2(-m_ref, -m_ref), a0, a1);
+                  float ra[4] = {0.f, 0.f, 0.f, 0.f};
+                  exp_body(std::true_type{}, std::true_type{}, f2(sl2, sl2), f2(-m_ref, -m_ref), a0, a1, ra);
                   const uint64_t hs = f2_add(a0, a1);
                   const float half_sum = f2_lo(hs) + f2_hi(hs);
                   if (!__any_sync(0xffffffffu, valid && !(half_sum <= 256.0f))) {
@@ -663,6 +673,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                     ps[1] += f2_hi(a0);
                     ps[2] += f2_lo(a1);
                     ps[3] += f2_hi(a1);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) rs[q] += ra[q];
                     spec_done = true;
                   } else {
                     load_s(region + 64u * h);
@@ -704,10 +716,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                   tc_fence_after();
                   rescale_o(alpha);
 #pragma unroll
-                  for (int q = 0; q < 4; ++q) ps[q] *= alpha;
+                  for (int q = 0; q < 4; ++q) {
+                    ps[q] *= alpha;
+                    rs[q] *= alpha;
+                  }
                 }
                 if (need) {
                   l *= alpha;
+                  lr *= alpha;
                   m_ref = m_new;
                 }
               }
@@ -718,7 +734,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               const float nm = live ? -m_ref : NEG_INF;
               const uint64_t SL2 = f2(sl2, sl2), NM = f2(nm, nm);
               uint64_t acc0 = f2(ps[0], ps[1]), acc1 = f2(ps[2], ps[3]);
-              auto body = [&](auto use_poly) { exp_body(use_poly, std::false_type{}, SL2, NM, acc0, acc1); };
+              auto body = [&](auto use_poly) { exp_body(use_poly, std::false_type{}, SL2, NM, acc0, acc1, rs); };
               if (!F32 && full)
                 body(std::true_type{});
               else
@@ -760,7 +776,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             mbar_arrive(&bar[(h == 0 ? B_PHALF0 : B_PFULL0) + b]);
             if (row_id == 0) trace_ev(p, t + j, (h == 0 ? 8 : 9) + 4 * X);
           }
-          if (valid) l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+          if (valid) {
+            l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+            lr += F32 ? (ps[0] + ps[1]) + (ps[2] + ps[3]) : (rs[0] + rs[1]) + (rs[2] + rs[3]);
+          }
         }
       }
       // ---------------- epilogue: O / l -> out (or partial), lse
@@ -775,18 +794,19 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       float sc0, sc1 = 0.f, lse_v;
       int c4_begin = 0, c4_end = D / 32;
       if (u.has_b) {
-        sc0 = l > 0.f ? 1.0f / l : 0.f;
+        sc0 = lr > 0.f ? 1.0f / lr : 0.f;
         lse_v = l > 0.f ? (m_ref + __log2f(l)) * 0.69314718055994530942f : NEG_INF;
       } else {
-        float2* xch = reinterpret_cast<float2*>(smem + C::OFF_XCH);
-        xch[X * 128 + row_id] = make_float2(m_ref, l);
+        float4* xch = reinterpret_cast<float4*>(smem + C::OFF_XCH);
+        xch[X * 128 + row_id] = make_float4(m_ref, l, lr, 0.f);
         named_bar_sync(1, 256);
-        const float2 o = xch[(1 - X) * 128 + row_id];
-        const float mA = X ? o.x : m_ref, lA = X ? o.y : l, mB = X ? m_ref : o.x, lB = X ? l : o.y;
+        const float4 o = xch[(1 - X) * 128 + row_id];
+        const float mA = X ? o.x : m_ref, lA = X ? o.y : l, rA = X ? o.z : lr;
+        const float mB = X ? m_ref : o.x, lB = X ? l : o.y, rB = X ? lr : o.z;
         const float M = fmaxf(lA > 0.f ? mA : NEG_INF, lB > 0.f ? mB : NEG_INF);
         const float wA = lA > 0.f ? ex2(mA - M) : 0.f, wB = lB > 0.f ? ex2(mB - M) : 0.f;
-        const float L = lA * wA + lB * wB;
-        const float inv = L > 0.f ? 1.0f / L : 0.f;
+        const float L = lA * wA + lB * wB, LR = rA * wA + rB * wB;
+        const float inv = LR > 0.f ? 1.0f / LR : 0.f;
         sc0 = wA * inv;
         sc1 = wB * inv;
         lse_v = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
@@ -923,8 +943,7 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   const uint32_t box[3] = {(uint32_t)C::ATOM_ELEMS, 128u, 1u};
   pi_status s = encode_tmap_3d(&tmK, dt, k_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
-  s = encode_tmap_3d(&tmV, F32 ? dt : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, v_buf, dims, strides, box,
-                     CU_TENSOR_MAP_SWIZZLE_128B);
+  s = encode_tmap_3d(&tmV, dt, v_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
   // Q as a 2D (row = token * q_heads_stride + head, d) tensor for tile::gather4 (box {atom, 1})
   CUtensorMap tmQ;
@@ -935,14 +954,9 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   s = encode_tmap_2d(&tmQ, dt, q, qdims, qstrides, qbox, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
 
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    s = cuda_check(cudaFuncSetAttribute(packed_attention_kernel<D, F32>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
-                   "cudaFuncSetAttribute");
-    if (s != PI_OK) return s;
-    attr_set = true;
-  }
+  static std::atomic<int> smem_opt_in[kMaxDevices];   // per template instance and device
+  s = set_max_dynamic_smem(reinterpret_cast<const void*>(packed_attention_kernel<D, F32>), smem_opt_in, C::SMEM);
+  if (s != PI_OK) return s;
   const int64_t total = (int64_t)p.total_p + (int64_t)p.n_work_d * p.units_d;
   const int grid = (int)std::min<int64_t>(total, num_sms());
   packed_attention_kernel<D, F32><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ);

@@ -1,5 +1,6 @@
 #include "device_common.h"
 
+#include <atomic>
 #include <mutex>
 
 namespace pi {
@@ -46,32 +47,49 @@ pi_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void
   return encode_tmap(2, map, dtype, base, dims, strides_bytes, box, swizzle);
 }
 
+// Per-device caches are atomics: concurrent first calls on several host threads may both query
+// the (idempotent) attribute, never read a torn value.
 int num_sms() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (!cache[dev]) {
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int v = cache[dev].load(std::memory_order_acquire);
+  if (!v) {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = n > 0 ? n : 148;
+    v = n > 0 ? n : 148;
+    cache[dev].store(v, std::memory_order_release);
   }
-  return cache[dev];
+  return v;
 }
 
 pi_status require_sm100() {
-  static int cache[64] = {0};  // 0 unknown, 1 ok, 2 bad
+  static std::atomic<int> cache[kMaxDevices];  // 0 unknown, 1 ok, 2 bad
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(PI_ECUDA, "no CUDA device");
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (!cache[dev]) {
+  if (dev < 0 || dev >= kMaxDevices) return fail(PI_EUNSUP, "device ordinal beyond the library's table");
+  int v = cache[dev].load(std::memory_order_acquire);
+  if (!v) {
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-    cache[dev] = (major == 10 && minor == 0) ? 1 : 2;
+    v = (major == 10 && minor == 0) ? 1 : 2;
+    cache[dev].store(v, std::memory_order_release);
   }
-  if (cache[dev] != 1) return fail(PI_EUNSUP, "libpackinfer is built for sm_100a (B200) only");
+  if (v != 1) return fail(PI_EUNSUP, "libpackinfer is built for sm_100a (B200) only");
   return PI_OK;
+}
+
+pi_status set_max_dynamic_smem(const void* func, std::atomic<int>* done, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(PI_ECUDA, "no CUDA device");
+  if (dev < 0 || dev >= kMaxDevices) return fail(PI_EUNSUP, "device ordinal beyond the library's table");
+  if (done[dev].load(std::memory_order_acquire)) return PI_OK;
+  pi_status s = cuda_check(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                           "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+  if (s == PI_OK) done[dev].store(1, std::memory_order_release);
+  return s;
 }
 
 }  // namespace pi

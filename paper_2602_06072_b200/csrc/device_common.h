@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <string>
 
 #include "common.h"
@@ -22,6 +23,8 @@ pi_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void
                          const uint64_t dims[3], const uint64_t strides_bytes[2],
                          const uint32_t box[3], CUtensorMapSwizzle swizzle);
 
+constexpr int kMaxDevices = 64;
+
 // Number of SMs of the current device (cached per device).
 int num_sms();
 
@@ -32,5 +35,9 @@ inline pi_status cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return PI_OK;
   return fail(PI_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// Opts `func` into `bytes` of dynamic shared memory on the CURRENT device, once per device
+// (done[kMaxDevices]: one flag per device ordinal, owned by the caller's kernel instance).
+pi_status set_max_dynamic_smem(const void* func, std::atomic<int>* done, int bytes);
 
 }  // namespace pi

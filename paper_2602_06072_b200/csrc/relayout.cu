@@ -1,16 +1,14 @@
 // Contiguous memory consolidation (PackInfer §3.2; Alg. 1 Copy lines P:244/P:250).
 //
 // Gathers every copy-plan entry from the paged KV cache [num_blocks, page, Hkv, d] into the
-// group-contiguous buffers [hkv_count, buffer_tokens, d].  For bf16 caches V is stored as fp16
-// (exact for |v| < 65504, saturated beyond) so that the packed attention can multiply an fp16 P
-// (8x finer than bf16) with it; K is copied bitwise.  One warp per RL_TPW consecutive buffer
+// group-contiguous buffers [hkv_count, buffer_tokens, d]: K and V are copied bitwise (R-layout).
+// One warp per RL_TPW consecutive buffer
 // tokens (one 32-ary search for their copy entry): per token it reads the hkv_count*d contiguous
 // elements of all local heads of one paged slot (coalesced) and scatters them into the per-head
 // buffers.  Cells in a suffix's headroom (delta) are
 // written with zeros so every buffer cell is finite (the attention kernels read whole 128-key
 // tiles; masked keys meet P = 0, which must not multiply NaN garbage).
 // HBM-bound: algorithmic bytes = 2 (K,V) x copied tokens x hkv_count x d x elem (read + write).
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,20 +36,7 @@ struct RelayoutParams {
   int64_t buf_head_bytes;     // buffer_tokens * d * es
   uint8_t* kb;
   uint8_t* vb;
-  int32_t v_to_f16;           // bf16 caches: convert V to fp16 on the way
 };
-
-__device__ __forceinline__ uint4 bf16x8_to_f16x8(uint4 v) {
-  uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float lo = fminf(fmaxf(__uint_as_float(w[i] << 16), -65504.f), 65504.f);
-    const float hi = fminf(fmaxf(__uint_as_float(w[i] & 0xffff0000u), -65504.f), 65504.f);
-    __half2 h = __floats2half2_rn(lo, hi);
-    w[i] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
 
 #ifndef PI_RL_TPW
 #define PI_RL_TPW 1
@@ -119,7 +104,7 @@ __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
             const int h = i / p.head_chunks, cc = i % p.head_chunks;
             const int64_t d = h * p.buf_head_bytes + dst * row_bytes + (int64_t)cc * 16;
             *reinterpret_cast<uint4*>(p.kb + d) = kv[u];
-            *reinterpret_cast<uint4*>(p.vb + d) = p.v_to_f16 ? bf16x8_to_f16x8(vv[u]) : vv[u];
+            *reinterpret_cast<uint4*>(p.vb + d) = vv[u];
           }
         }
       }
@@ -141,8 +126,7 @@ __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
 __global__ void __launch_bounds__(256) append_kernel(const int32_t* __restrict__ append_pos, int32_t n,
                                                       const uint8_t* kn, const uint8_t* vn, int64_t token_bytes,
                                                       int64_t head_off_bytes, int32_t chunks, int32_t head_chunks,
-                                                      int64_t buf_head_bytes, uint8_t* kb, uint8_t* vb,
-                                                      int32_t v_to_f16) {
+                                                      int64_t buf_head_bytes, uint8_t* kb, uint8_t* vb) {
   const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -157,7 +141,7 @@ __global__ void __launch_bounds__(256) append_kernel(const int32_t* __restrict__
     const uint4 kv = reinterpret_cast<const uint4*>(ks)[c];
     const uint4 vv = reinterpret_cast<const uint4*>(vs)[c];
     *reinterpret_cast<uint4*>(kb + d) = kv;
-    *reinterpret_cast<uint4*>(vb + d) = v_to_f16 ? bf16x8_to_f16x8(vv) : vv;
+    *reinterpret_cast<uint4*>(vb + d) = vv;
   }
 }
 
@@ -184,8 +168,7 @@ extern "C" pi_status packinfer_append_kv(const pi_device_plan* dp, const void* k
   append_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       dp->append_pos, dp->n_requests, static_cast<const uint8_t*>(k_new), static_cast<const uint8_t*>(v_new),
       (int64_t)hkv_total * head_dim * es, (int64_t)hkv_begin * head_dim * es, hkv_count * head_chunks, head_chunks,
-      dp->buffer_tokens * head_dim * es, static_cast<uint8_t*>(k_buf), static_cast<uint8_t*>(v_buf),
-      dt == PI_BF16 ? 1 : 0);
+      dp->buffer_tokens * head_dim * es, static_cast<uint8_t*>(k_buf), static_cast<uint8_t*>(v_buf));
   pi_status s = cuda_check(cudaGetLastError(), "append_kernel launch");
   return s == PI_OK ? ok() : s;
 }
@@ -226,7 +209,6 @@ extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void*
   p.buf_head_bytes = dp->buffer_tokens * head_dim * es;
   p.kb = static_cast<uint8_t*>(k_buf);
   p.vb = static_cast<uint8_t*>(v_buf);
-  p.v_to_f16 = dt == PI_BF16 ? 1 : 0;
   const int64_t blocks = (p.total + 8 * RL_TPW - 1) / (8 * RL_TPW);
   if (blocks > 0x7fffffff) return fail(PI_EINVAL, "buffer too large");
   relayout_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);

@@ -228,6 +228,15 @@ __device__ __forceinline__ uint32_t pack_f16(float a, float b) {
   __half2 v = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// a += lo half, b += hi half of a packed bf16x2 word, in fp32 (mixed-precision add, PTX ISA 8.6:
+// one FHADD.BF16 each, the half selected by the register operand; no unpacking instructions).
+__device__ __forceinline__ void add_bf16x2(float& a, float& b, uint32_t w) {
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+      "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+      : "+f"(a), "+f"(b)
+      : "r"(w));
+}
+
 // Instruction descriptor with separate A / B formats (kind::f16: 0 = f16, 1 = bf16).
 __host__ __device__ constexpr uint32_t idesc_make2(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N,
                                                    uint32_t a_mn_major, uint32_t b_mn_major) {

@@ -359,13 +359,18 @@ class PackedBatch:
         self._events[0].record()
         bt = max(int(c.buffer_tokens), 1)
         self.k_buf = torch.empty((hkv_count, bt, head_dim), dtype=dtype, device=self.device)
-        # bf16 caches keep V as fp16 in the group buffer (include/packinfer.h)
-        self.v_buf = torch.empty((hkv_count, bt, head_dim), dtype=torch.float16 if dtype == torch.bfloat16 else dtype,
-                                 device=self.device)
-        hq = hkv_count * gqa_ratio
-        ns = max(int(c.n_partial_slots), 1)
-        self.partial_o = torch.empty((ns, hq, head_dim), dtype=torch.float32, device=self.device)
-        self.partial_lse = torch.empty((ns, hq), dtype=torch.float32, device=self.device)
+        self.v_buf = torch.empty((hkv_count, bt, head_dim), dtype=dtype, device=self.device)
+        self.partial_o = self.partial_lse = None
+        self._ensure_partials()
+
+    def _ensure_partials(self):
+        """partial_o / partial_lse hold at least the current plan's n_partial_slots rows."""
+        import torch
+        ns = max(int(self.plan.c.n_partial_slots), 1)
+        if self.partial_o is None or self.partial_o.shape[0] < ns:
+            hq = self.hkv * self.r
+            self.partial_o = torch.empty((ns, hq, self.d), dtype=torch.float32, device=self.device)
+            self.partial_lse = torch.empty((ns, hq), dtype=torch.float32, device=self.device)
 
     def replan(self, stream=None, appended=None):
         """Host planning + plan upload (the per-step host part of the hot path).  `appended`:
@@ -383,6 +388,9 @@ class PackedBatch:
         if int(self.plan.c.arena_bytes) > self.dev_arena.numel():
             self.dev_arena = torch.empty(int(self.plan.c.arena_bytes), dtype=torch.uint8, device=self.device)
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
+        # appended tokens can push a decode suffix across a decode_chunk boundary: more decode items,
+        # more partial slots (the kernels index partial_o / partial_lse by the plan's slot ids)
+        self._ensure_partials()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream() if stream is None else stream)
         self._events[s] = ev

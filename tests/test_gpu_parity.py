@@ -36,13 +36,51 @@ def test_relayout_bitwise(C, delta):
     for buf_gpu, src in ((pb.k_buf, "k_paged"), (pb.v_buf, "v_paged")):
         want, valid = OL.expected_buffers(op.copies, t[src].cpu(), t["block_table"].cpu(), b.n, b.page_size,
                                           op.buffer_tokens)
-        if src == "v_paged":
-            # V is kept as fp16 in the group buffer (exact for |v| < 65504; R13)
-            f = (want.astype(np.uint16).astype(np.uint32) << 16).view(np.float32)
-            want = np.clip(f, -65504, 65504).astype(np.float16).view(np.int16)
         got = buf_gpu.cpu().view(torch.int16).numpy()
         assert np.array_equal(got[:, valid], want[:, valid])
         assert (got[:, ~valid] == 0).all()           # headroom zero-filled
+
+
+def test_relayout_bitwise_full_bf16_range():
+    """K and V cells are bitwise copies over the whole finite bf16 range: values far outside fp16
+    (|x| up to 3e38, subnormal bf16 down to 1e-40) and signed zeros survive the relayout."""
+    b = W.random_batch(3, n=9, max_len=400, hq=4, hkv=2, d=128, n_prefix=1)
+    t = W.make_tensors(b, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    for name in ("k_paged", "v_paged"):
+        x = t[name].float()
+        e = torch.randint(-133, 127, x.shape, generator=g, device="cuda").float()   # exponents incl. subnormal
+        t[name] = (x * torch.exp2(e)).to(torch.bfloat16)
+        t[name].view(-1)[:7] = torch.tensor([0.0, -0.0, 1e-40, -3e38, 65520.0, 1e5, 6e-8],
+                                            device="cuda").to(torch.bfloat16)
+    assert torch.isfinite(t["v_paged"].float()).all()
+    _, _, pb = H.run_batch(b, t, C=256, delta=3)
+    op = OP.plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, 256, headroom=3)
+    for buf_gpu, src in ((pb.k_buf, "k_paged"), (pb.v_buf, "v_paged")):
+        want, valid = OL.expected_buffers(op.copies, t[src].cpu(), t["block_table"].cpu(), b.n, b.page_size,
+                                          op.buffer_tokens)
+        got = buf_gpu.cpu().view(torch.int16).numpy()
+        assert np.array_equal(got[:, valid], want[:, valid])
+
+
+@pytest.mark.parametrize("k", [17, -20])
+def test_v_scale_equivariance(k):
+    """Attention is linear in V (o(q, K, c V) = c o(q, K, V), the oracle's definition): scaling V by
+    2^k (|v| ~ 1e5 for k = 17, far beyond fp16; ~1e-6 for k = -20, fp16-subnormal) scales every output
+    exactly — bf16 P x bf16 V with fp32 accumulation commutes with a power-of-two scale — and the
+    scaled outputs meet the gate after dividing by 2^k."""
+    b = W.random_batch(13, n=10, max_len=700, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=0.4)
+    t = W.make_tensors(b, device="cuda")
+    o1, l1, _ = H.run_batch(b, t, C=300, decode_chunk=256, out_f32=True)
+    ts = dict(t)
+    ts["v_paged"] = (t["v_paged"].float() * 2.0 ** k).to(torch.bfloat16)
+    assert torch.equal(ts["v_paged"].float(), t["v_paged"].float() * 2.0 ** k)   # exact in bf16
+    o2, l2, _ = H.run_batch(b, ts, C=300, decode_chunk=256, out_f32=True)
+    assert torch.equal(o2, o1 * 2.0 ** k)
+    assert torch.equal(l2, l1)
+    ro, rl = H.oracle_full(b, ts)
+    H.compare(o2 * 2.0 ** -k, l2, ro * 2.0 ** -k, rl)
 
 
 @pytest.mark.parametrize("delta", [0, 5])
@@ -82,10 +120,9 @@ def test_toy_fp32(maker, C, chunk):
     H.compare(out, lse, ro, rl, lse_tol=5e-3)
 
 
-@pytest.mark.parametrize("out_f32", [False, True])
 @pytest.mark.parametrize("seed", range(8))
 @pytest.mark.parametrize("d", [64, 128])
-def test_random_mixed_bf16(seed, d, out_f32):
+def test_random_mixed_bf16(seed, d):
     rng = np.random.default_rng(seed)
     hkv = int(rng.choice([1, 2, 4]))
     r = int(rng.choice([1, 4, 8]))
@@ -93,8 +130,7 @@ def test_random_mixed_bf16(seed, d, out_f32):
                        hkv=hkv, d=d, n_prefix=2, page_size=128 if seed % 2 else 256)
     C = int(rng.choice([8192, 512, 200]))
     t = W.make_tensors(b, device="cuda")
-    out, lse, _ = H.run_batch(b, t, C=C, delta=int(rng.integers(0, 9)), decode_chunk=128 * int(rng.integers(1, 4)),
-                              out_f32=out_f32)
+    out, lse, _ = H.run_batch(b, t, C=C, delta=int(rng.integers(0, 9)), decode_chunk=128 * int(rng.integers(1, 4)))
     ro, rl = H.oracle_full(b, t)
     H.compare(out, lse, ro, rl)
 
@@ -121,10 +157,24 @@ def test_peaky_queries():
     """q x 4 stresses the max-subtraction / lazy rescale path."""
     b = W.random_batch(77, n=8, max_len=800, hq=8, hkv=2, d=128)
     t = W.make_tensors(b, device="cuda", peaky=4.0)
-    for out_f32 in (False, True):
-        out, lse, _ = H.run_batch(b, t, C=300, decode_chunk=256, out_f32=out_f32)
-        ro, rl = H.oracle_full(b, t)
-        H.compare(out, lse, ro, rl)
+    ro, rl = H.oracle_full(b, t)
+    o32, l32, _ = H.run_batch(b, t, C=300, decode_chunk=256, out_f32=True)
+    H.compare(o32, l32, ro, rl)
+    o16, l16, _ = H.run_batch(b, t, C=300, decode_chunk=256, out_f32=False)
+    H.assert_bf16_is_rne_of_f32(o16, o32)
+    assert torch.equal(l16, l32)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_bf16_output_is_rne_of_f32(seed):
+    """The bf16-output mode differs from the fp32-output mode only by the final RNE store (prefill
+    epilogue, decode epilogue and merge), bit for bit."""
+    b = W.random_batch(500 + seed, n=14, max_len=900, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=0.4)
+    t = W.make_tensors(b, device="cuda")
+    o32, l32, _ = H.run_batch(b, t, C=384, delta=2, decode_chunk=256, out_f32=True)
+    o16, l16, _ = H.run_batch(b, t, C=384, delta=2, decode_chunk=256, out_f32=False)
+    H.assert_bf16_is_rne_of_f32(o16, o32)
+    assert torch.equal(l16, l32)
 
 
 @pytest.mark.parametrize("seed", [5, 6])
@@ -187,7 +237,7 @@ def test_mask_probe():
     for i in range(b.n):
         for j in range(-(-int(b.kv_len[i]) // b.page_size)):
             t["v_paged"][int(bt[i, j]), :, :, 0] = float(i)
-    out, lse, _ = H.run_batch(b, t, C=256, decode_chunk=128)
+    out, lse, _ = H.run_batch(b, t, C=256, decode_chunk=128, out_f32=False)   # integers: exact in bf16
     o = out.float().cpu().numpy()
     l = lse.cpu().numpy()
     off = 0
@@ -345,7 +395,7 @@ def test_decode_group_sharding_one_batch(world):
         vb = torch.zeros_like(pb.v_buf)
         pk.packinfer_relayout_kv(rp.dp, t["k_paged"], t["v_paged"], t["block_table"], kb, vb, 0, b.hkv)
         po, pl = torch.empty_like(pb.partial_o), torch.empty_like(pb.partial_lse)
-        out = torch.empty((b.total_q, b.hq, b.d), dtype=t["q"].dtype, device="cuda")
+        out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.float32, device="cuda")
         lse = torch.empty((b.hq, b.total_q), dtype=torch.float32, device="cuda")
         shard.init_partials(po, pl, out, lse)
         pk.packinfer_attention_decode(rp.dp, t["q"], kb, vb, out, lse, po, pl, r)
@@ -354,7 +404,7 @@ def test_decode_group_sharding_one_batch(world):
     # the all-reduces of shard.combine
     po = torch.stack(po_all).sum(0)
     pl = torch.stack(pl_all).amax(0)
-    out = torch.stack(out_all).float().sum(0).to(t["q"].dtype)
+    out = torch.stack(out_all).sum(0)              # exactly one rank wrote each row (others 0)
     lse = torch.stack(lse_all).amax(0)
     pk.packinfer_merge(pb.dp, po, pl, out, lse)
     torch.cuda.synchronize()
@@ -365,3 +415,40 @@ def test_decode_group_sharding_one_batch(world):
     torch.cuda.synchronize()
     union = torch.stack([k.view(torch.int16) for k in kbuf]).sum(0, dtype=torch.int64)
     assert torch.equal(union, pb.k_buf.view(torch.int16).to(torch.int64))
+
+
+def test_replan_grows_partials():
+    """Appended decode tokens that cross a decode_chunk boundary add decode items and partial slots
+    (plan_step); the batch's partial buffers grow with the plan and the result stays exact."""
+    from paper_2602_06072_b200 import packinfer as pk
+    chunk, delta = 256, 6
+    kv = np.array([chunk - 2, 2 * chunk - 1, 3 * chunk - 3, 40], np.int32)
+    b = W.Batch("chunk-edge", kv, np.ones(4, np.int32), np.full(4, -1, np.int32), np.zeros(0, np.int32),
+                8, 2, 128, "bf16", 128, 21)
+    t = W.make_tensors(b, device="cuda", extra_tokens=delta)
+    r = b.hq // b.hkv
+    pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16, "cuda",
+                        capacity=8192, headroom=delta, decode_chunk=chunk)
+    pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], torch.empty_like(t["q"]))
+    slots0 = int(pb.plan.c.n_partial_slots)
+    bt = t["block_table"].cpu().numpy()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    for k in range(1, delta + 1):
+        kn = torch.randn((b.n, b.hkv, b.d), generator=g, device="cuda").to(torch.bfloat16)
+        vn = torch.randn((b.n, b.hkv, b.d), generator=g, device="cuda").to(torch.bfloat16)
+        for i in range(b.n):
+            j = int(b.kv_len[i]) + k - 1
+            t["k_paged"][int(bt[i, j // b.page_size]), j % b.page_size] = kn[i]
+            t["v_paged"][int(bt[i, j // b.page_size]), j % b.page_size] = vn[i]
+        pb.append(kn, vn)
+        pb.replan(appended=np.full(b.n, k, np.int32))
+        assert pb.partial_o.shape[0] >= int(pb.plan.c.n_partial_slots)
+        out = torch.full((b.n, b.hq, b.d), float("nan"), dtype=torch.float32, device="cuda")
+        lse = torch.empty((b.hq, b.n), dtype=torch.float32, device="cuda")
+        pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out, lse, relayout=False)
+        torch.cuda.synchronize()
+        ro, rl = OA.attention(t["q"].cpu(), t["k_paged"].cpu(), t["v_paged"].cpu(), t["block_table"].cpu(),
+                              b.kv_len + k, b.q_len, b.page_size)
+        H.compare(out, lse, ro, rl)
+    assert int(pb.plan.c.n_partial_slots) > slots0

@@ -244,3 +244,109 @@ def test_cfg4_prefix_colocation():
     ideal = int(b.prefix_len.sum() + (b.kv_len - 2048).sum())
     assert ideal < pl.io_volume() < 0.5 * naive
     assert sum(1 for c in pl.copies if c.src_kind == 1) <= 64
+
+
+# ---------------------------------------------------------------- further pins (round 2)
+def test_eta_group_eq1():
+    """Eq. 1 left side: eta(S_g) = sum_{i in S_g} L_i^2 / T^2 — SPEC S:131-133's printed
+    values (two 64-token requests in one 128-tile group: 0.5; one 128-token request: 1.0) — and the
+    right side of the same equation: eta_batch = sum_g eta(S_g) / G for any partition."""
+    assert P.eta_group([64, 64], 128) == Fraction(1, 2)
+    assert P.eta_group([128], 128) == 1
+    assert P.eta_group([], 128) == 0
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        kv = [int(x) for x in rng.integers(1, 400, size=int(rng.integers(1, 25)))]
+        pl = _plan(kv, 500)
+        per_group = [P.eta_group([pl.pieces[k].kv_len for k in g.members], 128) for g in pl.groups]
+        assert sum(per_group) / len(pl.groups) == P.eta_batch(kv, len(pl.groups), 128)
+
+
+def test_num_groups_override_hand_traces():
+    """Alg. 1 line 1 with G supplied by the caller (num_groups, reading R2); hand traces on
+    SPEC's instance [100, 80, 60, 40], C = 150 (natural G0 = 2):
+      G = 3: 100 -> S0 (resulting 100 everywhere, lowest g); 80 -> S1 (S0: 180 > 150; S1 = S2 = 80);
+             60 -> S2 (S0: 160 > 150; S1 140, S2 60); 40 -> argmin(140, 120, 100) = S2.
+             Loads [100, 80, 100].
+      G = 1: 100 -> S0; 80 infeasible (180 > 150) -> opens S1; 60 -> S1 (140; S0 would be
+             160 > 150); 40 -> S0 (140; S1 would be 180).  Loads [140, 140], G grows 1 -> 2."""
+    pl = _plan([100, 80, 60, 40], 150, num_groups=3)
+    assert pl.G0 == 3
+    assert [sorted(pl.pieces[k].request for k in g.members) for g in pl.groups] == [[0], [1], [2, 3]]
+    assert [g.load for g in pl.groups] == [100, 80, 100]
+    pl = _plan([100, 80, 60, 40], 150, num_groups=1)
+    assert pl.G0 == 1
+    assert [sorted(pl.pieces[k].request for k in g.members) for g in pl.groups] == [[0, 3], [1, 2]]
+    assert [g.load for g in pl.groups] == [140, 140]
+    # with G = 2 supplied the trace is SPEC's own
+    pl = _plan([100, 80, 60, 40], 150, num_groups=2)
+    assert [g.load for g in pl.groups] == [140, 140]
+
+
+def test_prefix_argmin_two_group_hand_trace():
+    """Reading R1 (argmin of the RESULTING load load_g + L^_i with L^_i = L_i - L^g_shared,i)
+    on a batch whose prefix P0 (100 tokens) ends up in two groups.  C = 300, q_len = 1.
+      r0 = P0+80 (180), r1 = 170 (no prefix), r2 = P0+60 (160), r3 = P0+20 (120), r4 = P0+90 (190)
+      L_dedup = 820 - 3*100 = 520  ->  G0 = 2
+      r4 190 -> S0 (tie, lowest g)                                   loads [190, 0]
+      r0 180: S0 190+80 = 270, S1 0+180 = 180           -> S1          loads [190, 180]
+      r1 170: S0 360 > 300, S1 350 > 300                -> opens S2    loads [190, 180, 170]
+      r2 160: S0 190+60 = 250, S1 180+60 = 240, S2 330  -> S1          loads [190, 240, 170]
+      r3 120: S0 190+20 = 210, S1 260, S2 290           -> S0          loads [210, 240, 170]
+    Part 2 (R7-R9): S0 = [P0 | r4's 90 | r3's 20], S1 = [P0 | r0's 80 | r2's 60], S2 = [r1]."""
+    kv = [180, 170, 160, 120, 190]
+    pl = _plan(kv, 300, pid=[0, -1, 0, 0, 0], plen=[100])
+    assert pl.G0 == 2
+    assert [pl.pieces[k].request for k in pl.order] == [4, 0, 1, 2, 3]
+    assert [sorted(pl.pieces[k].request for k in g.members) for g in pl.groups] == [[3, 4], [0, 2], [1]]
+    assert [g.load for g in pl.groups] == [210, 240, 170]
+    assert [g.base for g in pl.groups] == [0, 210, 450] and pl.buffer_tokens == 620
+    off = {pl.pieces[k].request: tuple(pl.offsets[k]) for k in range(len(pl.pieces))}
+    assert off == {4: (0, 100, 100, 90), 3: (0, 100, 190, 20), 0: (0, 100, 100, 80), 2: (0, 100, 180, 60),
+                   1: (0, 0, 0, 170)}
+    assert [(c.src_kind, c.src_id, c.src_begin, c.length, c.dst) for c in pl.copies] == [
+        (1, 0, 0, 100, 0), (0, 4, 100, 90, 100), (0, 3, 100, 20, 190),
+        (1, 0, 0, 100, 210), (0, 0, 100, 80, 310), (0, 2, 100, 60, 390), (0, 1, 0, 170, 450)]
+    # Eq. 5: two prefix copies, below the naive per-request sum
+    assert pl.io_volume() == 620 < sum(kv)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_greedy_step_replay(seed):
+    """SPEC S:152 "Greedy step property": replaying the assignment order against the plan's own
+    final membership, every piece landed in a group that was feasible for it at that moment and had
+    the least resulting load among the feasible groups (lowest index on ties), or opened a new group
+    exactly when none was feasible.  The replay rebuilds the intermediate loads from the output
+    (groups' member lists + order), not from the oracle's loop."""
+    rng = np.random.default_rng(3000 + seed)
+    C = int(rng.integers(64, 600))
+    delta = int(rng.integers(0, 4))
+    mem = 0 if seed % 2 else C + delta + int(rng.integers(0, 300))
+    kv, q, pid, plen = _random_instance(rng, int(rng.integers(2, 40)), C)
+    G_in = int(rng.integers(1, 5)) if seed % 4 == 0 else 0
+    pl = P.plan(kv, q, pid, plen, C, mem_cap=mem, headroom=delta, num_groups=G_in)
+    where = {k: g for g, grp in enumerate(pl.groups) for k in grp.members}
+    loads = [0] * pl.G0
+    members = [0] * pl.G0
+    held = [set() for _ in range(pl.G0)]
+    for k in pl.order:
+        pc = pl.pieces[k]
+        contrib = [pc.kv_len - (plen[pc.prefix] if pc.prefix >= 0 and pc.prefix in held[g] else 0)
+                   for g in range(len(loads))]
+        feas = [g for g in range(len(loads)) if loads[g] + contrib[g] <= C and
+                (mem == 0 or loads[g] + contrib[g] + delta * (members[g] + 1) <= mem)]
+        g = where[k]
+        if feas:
+            best = min(feas, key=lambda x: (loads[x] + contrib[x], x))
+            assert g == best, (k, g, best)
+        else:
+            assert g == len(loads)              # a new group, opened at the end (P:230)
+            loads.append(0)
+            members.append(0)
+            held.append(set())
+            contrib.append(pc.kv_len)
+        loads[g] += contrib[g]
+        members[g] += 1
+        if pc.prefix >= 0:
+            held[g].add(pc.prefix)
+    assert loads == [grp.load for grp in pl.groups]

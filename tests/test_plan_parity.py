@@ -190,3 +190,21 @@ def test_deterministic_bytes():
     a2 = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, pk.default_config(headroom=32))
     assert a1.c.arena_bytes == a2.c.arena_bytes
     assert bytes(a1.arena) == bytes(a2.arena)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 7])
+def test_num_groups_override_bit_exact(G):
+    """num_groups (Alg. 1 line 1 override) above and below the natural G0, on the hand-traced
+    instance of tests/test_oracle_plan.py and on a prefix batch."""
+    hp, op = _both([100, 80, 60, 40], [1] * 4, None, [], 150, G=G)
+    assert hp.c.g0 == G
+    assert_bit_exact(hp, op)
+    b = W.random_batch(17, n=30, max_len=900, n_prefix=3)
+    hp, op = _both(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, 700, G=G, delta=3)
+    assert_bit_exact(hp, op)
+
+
+def test_prefix_two_group_trace_bit_exact():
+    hp, op = _both([180, 170, 160, 120, 190], [1] * 5, [0, -1, 0, 0, 0], [100], 300)
+    assert_bit_exact(hp, op)
+    assert [int(g["load"]) for g in hp.groups] == [210, 240, 170]
