@@ -3,17 +3,20 @@
 vs B200 peak; batch step latency).
 
 One STEP = one pass of the whole hot path over one batch:
-    packinfer_plan (host C++) -> plan upload (H2D) -> packinfer_relayout_kv -> packed prefill
-    -> packed decode -> LSE merge
+    packinfer_plan (host C++) -> plan upload (H2D + device row expansion) -> packinfer_relayout_kv
+    -> packed prefill -> packed decode -> LSE merge
 Headline workload (N=1): BASELINE.json configs[1], the Llama-3-8B-shaped heterogeneous prefill
 batch (64 requests, 16..8192 tokens; 32 Q / 8 KV heads, d=128, bf16).  value = algorithmic
-prefill FLOPs / step time (TFLOP/s).  The decode row (configs[2], 256 requests, KV 32..32k) is
-reported under "decode" (GB/s of Eq. 5 KV bytes).
+prefill FLOPs / step time (TFLOP/s).  Side sections: configs[2] decode (GB/s of Eq. 5 KV bytes),
+configs[3] shared-prefix decode + suffix prefill, configs[4] mixed 70B batch (one fused launch),
+the decode loop (NEXT-1) with the online capacity tuner (NEXT-2), planner host microseconds.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--shard group|heads]
-Multi-GPU (torchrun, one process per GPU): default --shard group = weak scaling, rank r runs
-its own batch (seed 0 + r; groups of independent sub-batches, no collective on the data path);
---shard heads = strong scaling by KV head over one batch.
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--shard heads|group]
+--gpus N > 1 without a torchrun environment re-launches itself under torchrun (one process per
+GPU, 127.0.0.1 rendezvous).  --shard heads (default) = STRONG scaling: every rank runs the same
+batch on its KV-head share (no collective on the data path), value = the batch's FLOPs / max-over-
+ranks step time, and the line carries strong_scaling = T(1) / (N T(N)) measured in the same run.
+--shard group = weak scaling: rank r runs its own batch (seed + r).
 """
 
 from __future__ import annotations
@@ -45,58 +48,74 @@ def load_peaks():
 
 # ------------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi every 10 ms in a background thread; summaries cover only the samples taken
+    inside a given host-time window (the timed region), so idle or set-up periods never enter
+    the reported clock."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, interval_ms: int = 10):
         self.idx = gpu_index
+        self.interval_ms = interval_ms
         self.proc = None
-        self.lines = []
+        self.samples = []          # (host time, sm MHz, max MHz, power W, reasons)
         self.thread = None
 
-    def start(self):
+    def start(self, wait_s: float = 3.0):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < wait_s:   # first sample = sampler running
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        self.thread.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+            f = [x.strip() for x in line.strip().split(",")]
             if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx.append(float(f[2]))
+                sm, mx = float(f[1]), float(f[2])
+                pw = float(f[3]) if f[3] not in ("[N/A]", "") else None
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+            reasons = {n for n, v in zip(self.NAMES, f[5:9]) if v.lower() == "active"}
+            self.samples.append((time.time(), sm, mx, pw, reasons))
+
+    def window(self, t0: float, t1: float):
+        """Clock summary of the samples taken in [t0, t1] (host time)."""
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        inside = [x for x in list(self.samples) if t0 <= x[0] <= t1]
+        if not inside:
+            # region shorter than one sampling interval: the sample closest to its middle
+            mid = 0.5 * (t0 + t1)
+            allx = list(self.samples)
+            if not allx:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            inside = [min(allx, key=lambda x: abs(x[0] - mid))]
+        reasons = sorted(set().union(*[x[4] for x in inside]))
+        pw = [x[3] for x in inside if x[3] is not None]
+        return {"sm_mhz": statistics.median(x[1] for x in inside), "sm_max_mhz": max(x[2] for x in inside),
+                "sm_mhz_min": min(x[1] for x in inside), "power_w_median": statistics.median(pw) if pw else None,
+                "reasons": reasons, "samples": len(inside), "interval_ms": self.interval_ms,
+                "window_ms": (t1 - t0) * 1e3}
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
 
 
 # ------------------------------------------------------------------------------- workloads
@@ -108,6 +127,10 @@ def make_workload(name: str, seed: int):
         return W.cfg3_decode(seed + 1)
     if name == "cfg4_decode":
         return W.cfg4_decode(seed + 2)
+    if name == "cfg4_prefill":
+        return W.cfg4_prefill(seed + 2)
+    if name == "cfg5":
+        return W.cfg5_mixed(seed + 3)
     raise ValueError(name)
 
 
@@ -162,7 +185,9 @@ class Runner:
         self.lse = torch.empty((hkv_count * self.r, b.total_q), dtype=torch.float32, device=device)
         self.stream = torch.cuda.current_stream()
         c = self.pbs[0].plan.c
-        self.launches_per_step = 1 + (c.n_prefill_work > 0) + (c.n_decode_work > 0) + (c.n_merges > 0)
+        # relayout + row expansion (inside the plan upload) + prefill + decode + merge
+        self.launches_per_step = 1 + (c.n_segs > 0) + (c.n_prefill_work > 0) + (c.n_decode_work > 0) + \
+            (c.n_merges > 0)
         self.kernel_events = []
         self.step_events = []
 
@@ -213,7 +238,10 @@ class Runner:
         return (sum(pre) / len(pre) if pre else 0.0), (sum(dec) / len(dec) if dec else 0.0)
 
 
-def timed_steps(runner, steps, warmup, dist_on):
+def timed_steps(runner, steps, warmup, dist_on, window=None):
+    """W untimed warm-up steps, then exactly `steps` steps between a barrier + synchronize on both
+    sides, timed with CUDA events on the step stream.  window (list): receives the host-time
+    bounds of the timed region (for the clock sampler)."""
     import torch
     for i in range(warmup):
         runner.step(i)
@@ -225,11 +253,15 @@ def timed_steps(runner, steps, warmup, dist_on):
     runner.kernel_events.clear()
     runner.step_events.clear()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
     s.record()
     for i in range(steps):
         runner.step(warmup + i, time_kernel=True)
     e.record()
     torch.cuda.synchronize()
+    t1 = time.time()
+    if window is not None:
+        window[:] = [t0, t1]
     if dist_on:
         import torch.distributed as dist
         dist.barrier()
@@ -346,6 +378,131 @@ def W_tensors(b, dev):
     return W.make_tensors(b, device=dev, seed=b.seed)
 
 
+def decode_loop(dev, h0, hc, seed_rank, args):
+    """Decode loop (NEXT-1) on configs[2]: consolidate once with headroom
+    delta = 32 (= max new tokens), then each step appends one token per request into its
+    headroom, re-plans the execution domain on the host (packinfer_plan_step) and runs decode +
+    merge.  Plus the online capacity tuner (NEXT-2) driving C on configs[3]."""
+    import torch
+    from synth import workloads as W
+    from paper_2602_06072_b200 import packinfer as pk
+    bd = make_workload("cfg3", seed_rank)
+    loop_steps, delta = 32, 32
+    tl = W.make_tensors(bd, device=dev, seed=bd.seed, extra_tokens=loop_steps)
+    rr = bd.hq // bd.hkv
+    pbl = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, rr, bd.d, torch.bfloat16, dev,
+                         headroom=delta)
+    ql = tl["q"][:, h0 * rr:(h0 + hc) * rr]
+    outl = torch.empty((bd.n, hc * rr, bd.d), dtype=torch.bfloat16, device=dev)
+    kn = torch.randn((bd.n, bd.hkv, bd.d), device=dev).to(torch.bfloat16)
+    vn = torch.randn_like(kn)
+
+    def loop_once():
+        pbl.replan()
+        pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0)   # consolidation
+        for k in range(1, loop_steps):
+            pbl.append(kn, vn, hkv_begin=h0)
+            pbl.replan(appended=np.full(bd.n, k, np.int32))
+            pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0, relayout=False)
+    loop_once()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    loop_once()
+    e1.record()
+    torch.cuda.synchronize()
+    lms = e0.elapsed_time(e1) / loop_steps
+    kv_tokens = sum(int(bd.kv_len.sum()) + k * bd.n for k in range(loop_steps)) / loop_steps
+    lbytes = 2 * kv_tokens * hc * bd.d * 2 + 2 * bd.n * hc * rr * bd.d * 2
+    out = {"workload": bd.name + " (BASELINE.json configs[2])", "steps": loop_steps, "headroom": delta,
+           "ms_per_step_amortized": lms, "step_gbs_amortized": lbytes / (lms * 1e-3) / 1e9,
+           "note": "consolidation (relayout) once per 32 steps; per step: append + plan_step + upload + "
+                   "decode attention + merge"}
+    del tl, pbl
+    out["tuned"] = tuned_loop(dev, h0, hc, seed_rank)
+    return out
+
+
+def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192, 16384)):
+    """NEXT-2 online refinement ("each decoding step naturally yields one performance
+    sample"): a decode loop over configs[3] (shared prefixes) whose capacity C is chosen by
+    tuning.CapacityTuner at every regroup point.  An epoch = consolidation with the tuner's C
+    (re-plan + relayout), then decode steps that append into the headroom until Eq. 4
+    triggers a regroup or the headroom is exhausted.  Every step is timed with CUDA events on its
+    stream (decode attention + merge + append); the samples (ms per KV token, read back one epoch
+    later without stalling the loop) feed tuner.observe(C, cost)."""
+    import torch
+    from synth import workloads as W
+    from paper_2602_06072_b200 import packinfer as pk
+    from paper_2602_06072_b200.tuning import CapacityTuner
+    bd = make_workload("cfg4_decode", seed_rank)
+    delta = 32
+    t = W.make_tensors(bd, device=dev, seed=bd.seed, extra_tokens=delta)
+    rr = bd.hq // bd.hkv
+    q = t["q"][:, h0 * rr:(h0 + hc) * rr]
+    out = torch.empty((bd.n, hc * rr, bd.d), dtype=torch.bfloat16, device=dev)
+    kn = torch.randn((bd.n, bd.hkv, bd.d), device=dev).to(torch.bfloat16)
+    vn = torch.randn_like(kn)
+    st = torch.cuda.current_stream()
+    tuner = CapacityTuner(list(cands), probe_every=4)
+    pending, history = [], []
+    batches = {}
+
+    def drain(block):
+        keep = []
+        for (c, ev0, ev1, kv) in pending:
+            if block or ev1.query():
+                ev1.synchronize()
+                tuner.observe(c, ev0.elapsed_time(ev1) / kv * 1e6)    # ns per KV token
+            else:
+                keep.append((c, ev0, ev1, kv))
+        pending[:] = keep
+
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(st)
+    total_steps = 0
+    for ep in range(epochs):
+        drain(block=False)
+        C = tuner.choose()
+        if C not in batches:
+            batches[C] = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, rr, bd.d,
+                                        torch.bfloat16, dev, capacity=C, headroom=delta)
+        pb = batches[C]
+        pb.replan(st)
+        pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf, pb.v_buf, h0, hc,
+                                 st)
+        k, steps = 0, 0
+        while True:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(st)
+            if k > 0:
+                pb.append(kn, vn, hkv_begin=h0, stream=st)
+                pb.replan(st, appended=np.full(bd.n, k, np.int32))
+            pb.run(q, t["k_paged"], t["v_paged"], t["block_table"], out, hkv_begin=h0, stream=st, relayout=False)
+            ev1.record(st)
+            kv = int(pb.plan.c.copy_tokens) + int(pb.plan.c.appended_total)
+            pending.append((C, ev0, ev1, kv))
+            steps += 1
+            k += 1
+            if k > delta - 1 or pk.packinfer_should_regroup(k, int(pb.plan.c.drift), C):
+                break
+        history.append({"epoch": ep, "capacity": C, "steps": steps, "groups": int(pb.plan.c.n_groups),
+                        "drift": int(pb.plan.c.drift)})
+        total_steps += steps
+    t_end.record(st)
+    drain(block=True)
+    torch.cuda.synchronize()
+    ms = t_start.elapsed_time(t_end) / max(1, total_steps)
+    res = {"workload": bd.name + " (BASELINE.json configs[3])", "candidates": list(cands), "epochs": history,
+           "ms_per_step": ms, "best_capacity": tuner.best(),
+           "cost_ns_per_kv_token": {str(c): tuner.mean[c] for c in tuner.cands},
+           "note": "C chosen by CapacityTuner at every regroup (Eq. 4 or headroom exhausted); samples = "
+                   "per-step CUDA-event time / KV tokens, fed back asynchronously"}
+    del t, batches
+    return res
+
+
 def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
     """BASELINE.json configs[4]: Llama-3-70B-shaped mixed batch (2 x 128k-token prefills split
     across groups + 30 short prefills + 224 decodes up to 32k), ONE fused attention launch over
@@ -419,29 +576,101 @@ def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
 
 
 # ------------------------------------------------------------------------------- oracle timing
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def stratified_requests(b, seed: int, strata: int = 8):
+    """Request order for the oracle sample: requests sorted by KV length are cut into `strata`
+    equal-count strata and the order takes one (seeded-random) request from each stratum in turn,
+    so any prefix of it covers short and long requests alike (the workload's length mix)."""
+    rng = np.random.default_rng(seed)
+    idx = np.argsort(b.kv_len, kind="stable")
+    parts = [list(rng.permutation(part)) for part in np.array_split(idx, strata) if len(part)]
+    order = []
+    while any(parts):
+        for part in parts:
+            if part:
+                order.append(int(part.pop()))
+    return order
+
+
 def oracle_sample(b, budget_s: float, seed: int):
-    """Times the oracle (as it stands) on a bounded sample of the workload's requests on this
-    host.  Returns (algorithmic FLOP/s or KV bytes/s, seconds, description, cores)."""
+    """Times the oracle (as it stands) on a bounded, stratified sample of the workload's requests on
+    this host: requests are taken in stratified_requests order until the budget is spent.  The
+    paged cache is upcast to fp64 once, outside the timed region (inputs resident, as for the GPU
+    arm).  Returns (algorithmic FLOPs, KV bytes, seconds, description, cores)."""
     import torch
     from oracle import attention as OA
     from synth import workloads as W
     cores = len(os.sched_getaffinity(0))
     t = W.make_tensors(b, device="cpu", seed=seed)
-    order = np.argsort(b.kv_len)                      # short requests first, then longer ones
-    done, flops, kv_bytes, t0 = [], 0, 0, time.time()
-    for i in order:
-        if time.time() - t0 > budget_s:
+    q64 = t["q"].to(torch.float64).numpy()
+    k64 = t["k_paged"].to(torch.float64).numpy()
+    v64 = t["v_paged"].to(torch.float64).numpy()
+    bt = t["block_table"].numpy()
+    done, flops, kv_bytes, secs = [], 0, 0, 0.0
+    for i in stratified_requests(b, seed):
+        if secs > budget_s:
             break
-        OA.attention(t["q"], t["k_paged"], t["v_paged"], t["block_table"], b.kv_len, b.q_len, b.page_size,
-                     requests=[int(i)])
+        t0 = time.perf_counter()
+        OA.attention(q64, k64, v64, bt, b.kv_len, b.q_len, b.page_size, requests=[i])
+        secs += time.perf_counter() - t0
         L, q = int(b.kv_len[i]), int(b.q_len[i])
         flops += 4 * b.d * b.hq * (q * (L - q) + q * (q + 1) // 2)
         kv_bytes += 2 * L * b.hkv * b.d * 2
-        done.append(int(i))
-    dt = time.time() - t0
-    desc = (f"{len(done)}/{b.n} requests of {b.name} (shortest first, {int(b.kv_len[done].sum())} KV tokens), "
-            f"fp64 numpy, {dt:.1f}s")
-    return flops, kv_bytes, dt, desc, cores
+        done.append(i)
+    lens = b.kv_len[done]
+    desc = (f"{len(done)}/{b.n} requests of {b.name}, stratified by KV length (8 strata, one request per "
+            f"stratum in turn; lengths {int(lens.min())}..{int(lens.max())}, {int(lens.sum())} KV tokens = "
+            f"{100.0 * lens.sum() / b.kv_len.sum():.1f}% of the batch), fp64 numpy, {secs:.1f}s; "
+            f"CPU: {cpu_model()}")
+    return flops, kv_bytes, secs, desc, cores
+
+
+def oracle_planner_us(reps: int = 3):
+    """Host microseconds of the oracle planner (oracle/plan.py, Alg. 1 Parts 1-2) on the BASELINE
+    configs, median of `reps` (the reference arm for the planner row)."""
+    from oracle import plan as OP
+    out = {}
+    for name in ("cfg2", "cfg3", "cfg4_decode", "cfg5"):
+        b = make_workload(name, 0)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            OP.plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, 8192)
+            ts.append((time.perf_counter() - t0) * 1e6)
+        out[name] = statistics.median(ts)
+    return out
+
+
+def planner_us(reps: int = 50):
+    """Host microseconds of packinfer_plan (C++, through the binding) per BASELINE config: median and
+    p90 over `reps` calls into a pre-sized pinned arena (the per-step host cost of the hot path)."""
+    from paper_2602_06072_b200 import packinfer as pk
+    out = {}
+    for name in ("cfg2", "cfg3", "cfg4_decode", "cfg5"):
+        b = make_workload(name, 0)
+        cfg = pk.default_config(capacity=8192, gqa_ratio=b.hq // b.hkv)
+        hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, cfg, pinned=True)
+        arena = hp.arena
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, cfg, arena=arena)
+            ts.append((time.perf_counter() - t0) * 1e6)
+        c = hp.c
+        out[name] = {"median_us": statistics.median(ts), "p90_us": float(np.percentile(ts, 90)),
+                     "pieces": int(c.n_pieces), "groups": int(c.n_groups), "row_segments": int(c.n_segs),
+                     "rows_expanded_on_device": int(c.n_rows), "host_arena_bytes": int(c.arena_bytes)}
+    return out
 
 
 def run_reference(args, cfg_name):
@@ -462,7 +691,8 @@ def run_reference(args, cfg_name):
     v = sum(vals) / len(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * sum(secs) / len(secs), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000 * sum(secs) / len(secs), "higher_is_better": True,
+            "scaling": "strong" if args.shard == "heads" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": arm_config(b, args.shard, args.gpus),
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
@@ -471,28 +701,122 @@ def run_reference(args, cfg_name):
 
 
 # ------------------------------------------------------------------------------- main
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torchrun with N processes (one per
+    GPU) on a 127.0.0.1 rendezvous and exit with its status.  Fails loudly when the box has fewer
+    than N GPUs (unless PI_BENCH_ONE_GPU=1 puts every rank on cuda:0, a test hook)."""
+    import socket
+    import torch
+    if os.environ.get("PI_BENCH_ONE_GPU") != "1" and os.environ.get("PI_BENCH_DRYRUN") != "1" and \
+            torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {torch.cuda.device_count()} CUDA devices"}),
+              flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def max_over_ranks(dev, *vals):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in vals], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_rank):
+    """A decode step (plan + upload + relayout + decode attention + merge) of one BASELINE batch on
+    this rank's KV heads; GB/s = Eq. 5 KV bytes + Q/O bytes over the decode kernel time."""
+    bd = make_workload(name, seed_rank)
+    rd = Runner(bd, dev, h0, hc, seed=bd.seed)
+    _, kvb, qob = algorithmic(bd, rd.pbs[0].plan.c, hc)
+    steps = max(10, args.steps)
+    win = []
+    dms = timed_steps(rd, steps, args.warmup, dist_on, win) / steps
+    _, dec_ms = rd.kernel_ms()
+    if dist_on:
+        dms, dec_ms = max_over_ranks(dev, dms, dec_ms)
+    ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
+    c = rd.pbs[0].plan.c
+    out = {"ms_per_step": dms, "kernel_ms": dec_ms, "kv_bytes": kvb, "qo_bytes": qob, "achieved_gbs": ach,
+           "peak_gbs": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
+           "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9, "work_items": int(c.n_decode_work),
+           "partial_slots": int(c.n_partial_slots), "groups": int(c.n_groups),
+           "step_latency": rd.step_latency(), "gpu_launches": rd.launches_per_step * steps,
+           "clocks": sampler.window(*win) if win else None}
+    del rd
+    return out
+
+
+def section_prefill(name, dev, h0, hc, args, peaks, dist_on, sampler, seed_rank):
+    """A prefill step of one BASELINE batch on this rank's KV heads (TFLOP/s over the prefill
+    kernel time and over the step)."""
+    bp = make_workload(name, seed_rank)
+    rp = Runner(bp, dev, h0, hc, seed=bp.seed)
+    flops, _, _ = algorithmic(bp, rp.pbs[0].plan.c, hc)
+    steps = max(10, args.steps)
+    win = []
+    pms = timed_steps(rp, steps, args.warmup, dist_on, win) / steps
+    pre_ms, _ = rp.kernel_ms()
+    if dist_on:
+        pms, pre_ms = max_over_ranks(dev, pms, pre_ms)
+    ach = flops / (pre_ms * 1e-3) / 1e12
+    c = rp.pbs[0].plan.c
+    out = {"ms_per_step": pms, "kernel_ms": pre_ms, "tflop": flops / 1e12, "achieved_tflops": ach,
+           "peak_tflops": peaks["bf16_tflops"], "frac": ach / peaks["bf16_tflops"], "bound": "tensor",
+           "step_tflops": flops / (pms * 1e-3) / 1e12, "work_items": int(c.n_prefill_work),
+           "groups": int(c.n_groups), "tile_efficiency": c.valid_cells / max(1, c.tile_cells),
+           "step_latency": rp.step_latency(), "gpu_launches": rp.launches_per_step * steps,
+           "clocks": sampler.window(*win) if win else None}
+    del rp
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="packinfer", choices=["packinfer", "reference"])
-    ap.add_argument("--shard", default="group", choices=["group", "heads"])
+    ap.add_argument("--shard", default="heads", choices=["heads", "group"])
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-prefix", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-loop", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-mixed", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args, "cfg2")
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args)
 
     import torch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N ranks for --gpus N)")
+    if os.environ.get("PI_BENCH_DRYRUN") == "1":
+        # test hook (CPU): the launch path only - ranks rendezvous over gloo, agree on the world
+        # size and the KV-head shards, and rank 0 prints them
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        from paper_2602_06072_b200 import shard
+        t = torch.tensor([1.0])
+        dist.all_reduce(t)
+        shards = [shard.kv_head_shard(8, q, world) for q in range(world)]
+        if rank == 0:
+            print(json.dumps({"dryrun": True, "world": world, "ranks_seen": int(t.item()), "kv_head_shards": shards}),
+                  flush=True)
+        dist.destroy_process_group()
+        return
     # test hook: PI_BENCH_ONE_GPU=1 puts every rank on cuda:0 with gloo (exercises the N > 1 code
     # path on a one-GPU box; never used for a reported number)
     one_gpu = os.environ.get("PI_BENCH_ONE_GPU") == "1"
@@ -508,9 +832,13 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peak_src = load_peaks()
     dev = torch.device("cuda", local)
+    sampler = ClockSampler(local)
+    sampler.start()
 
-    b = make_workload("cfg2", 0 if args.shard == "heads" else rank)
-    if args.shard == "heads" and world > 1:
+    heads = args.shard == "heads"
+    seed_rank = 0 if heads else rank
+    b = make_workload("cfg2", seed_rank)
+    if heads and world > 1:
         from paper_2602_06072_b200 import shard
         h0, hc = shard.kv_head_shard(b.hkv, rank, world)
     else:
@@ -518,19 +846,15 @@ def main():
     runner = Runner(b, dev, h0, hc, seed=b.seed)
     flops, _, _ = algorithmic(b, runner.pbs[0].plan.c, hc)
 
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
-    total_ms = timed_steps(runner, args.steps, args.warmup, dist_on)
-    clocks = sampler.stop()
+    win = []
+    total_ms = timed_steps(runner, args.steps, args.warmup, dist_on, win)
+    clocks = sampler.window(*win)
     ms_step = total_ms / args.steps
     pre_ms, _ = runner.kernel_ms()
     units_total = flops
     if dist_on:
         import torch.distributed as dist
-        tt = torch.tensor([ms_step, pre_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)           # step time = slowest rank
-        ms_step, pre_ms = float(tt[0]), float(tt[1])
+        ms_step, pre_ms = max_over_ranks(dev, ms_step, pre_ms)     # step time = slowest rank
         ft = torch.tensor([float(flops)], device=dev, dtype=torch.float64)
         dist.all_reduce(ft, op=dist.ReduceOp.SUM)           # work of every rank's shard / batch
         units_total = float(ft[0])
@@ -559,112 +883,82 @@ def main():
 
     result = {"metric": METRIC, "value": value, "unit": "TFLOP/s",
               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-              "higher_is_better": True, "scaling": "weak" if args.shard == "group" else "strong",
+              "higher_is_better": True, "scaling": "strong" if heads else "weak",
               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
               "config": arm_config(b, args.shard, world),
               "plan": {"groups": int(pc.n_groups), "work_items": int(pc.n_prefill_work),
-                       "step": "plan+upload+relayout+prefill(+decode+merge)",
+                       "row_segments": int(pc.n_segs), "rows": int(pc.n_rows),
+                       "step": "plan+upload(+row expansion)+relayout+prefill(+decode+merge)",
                        "algorithmic_tflop_per_rank": flops / 1e12},
               "roofline": roofline, "clocks": clocks, "step_latency": runner.step_latency(),
               "gpu_launches": runner.launches_per_step * args.steps}
+    del runner
 
-    if dist_on and args.shard == "heads":
+    if dist_on and heads:
+        # Strong scaling T(1) / (N T(N)) on the same batch, measured in this run: every rank also
+        # times the UNSHARDED step (all KV heads) on its own GPU; T(1) = the max over ranks.
+        r1 = Runner(b, dev, 0, b.hkv, seed=b.seed)
+        t1 = timed_steps(r1, args.steps, args.warmup, dist_on) / args.steps
+        (t1,) = max_over_ranks(dev, t1)
+        del r1
+        result["strong_scaling"] = {"t1_ms": t1, "tn_ms": ms_step, "n": world,
+                                    "efficiency": t1 / (world * ms_step)}
         # Full O on every rank (only for callers that need it; not part of the timed step): one
         # NCCL all-gather of the head-sharded outputs over NVLink.
         from paper_2602_06072_b200 import shard
         import torch.distributed as dist
-        shard.gather_heads(runner.out, world, b.hkv, runner.r)
+        rg = Runner(b, dev, h0, hc, seed=b.seed)
+        rg.step(0)
+        shard.gather_heads(rg.out, world, b.hkv, rg.r)
         torch.cuda.synchronize()
         dist.barrier()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 5
         g0.record()
         for _ in range(reps):
-            full = shard.gather_heads(runner.out, world, b.hkv, runner.r)
+            full = shard.gather_heads(rg.out, world, b.hkv, rg.r)
         g1.record()
         torch.cuda.synchronize()
-        gt = torch.tensor([g0.elapsed_time(g1) / reps], device=dev)
-        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        (gms,) = max_over_ranks(dev, g0.elapsed_time(g1) / reps)
         gbytes = full.numel() * full.element_size()
-        result["gather"] = {"ms": float(gt[0]), "bytes_out": gbytes,
-                            "step_ms_with_gather": ms_step + float(gt[0]),
+        result["gather"] = {"ms": gms, "bytes_out": gbytes, "step_ms_with_gather": ms_step + gms,
+                            "efficiency_with_gather": t1 / (world * (ms_step + gms)),
                             "note": "NCCL all_gather_into_tensor of head-major O slabs + layout copy"}
-        del full
+        del full, rg
 
     if not args.no_decode:
-        bd = make_workload("cfg3", 0 if args.shard == "heads" else rank)
-        rd = Runner(bd, dev, h0, hc, seed=bd.seed)
-        _, kvb, qob = algorithmic(bd, rd.pbs[0].plan.c, hc)
-        dms = timed_steps(rd, max(3, args.steps), args.warmup, dist_on) / max(3, args.steps)
-        _, dec_ms = rd.kernel_ms()
-        ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
+        d = section_decode("cfg3", dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_rank)
+        d["workload"] = "cfg3-llama3-8b-decode (BASELINE.json configs[2])"
         dtraffic = None
         if os.path.exists(tf):
             dtraffic = json.load(open(tf)).get("decode_attention_dram_bytes")
-        result["decode"] = {"workload": bd.name + " (BASELINE.json configs[2])", "ms_per_step": dms, "traffic": dtraffic,
-                            "kernel_ms": dec_ms, "kv_bytes": kvb, "achieved_gbs": ach, "peak_gbs": peaks["hbm_gbs"],
-                            "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
-                            "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9,
-                            "work_items": int(rd.pbs[0].plan.c.n_decode_work),
-                            "partial_slots": int(rd.pbs[0].plan.c.n_partial_slots),
-                            "step_latency": rd.step_latency()}
-        result["decode"]["gpu_launches"] = rd.launches_per_step * max(3, args.steps)
-        del rd
+        d["traffic"] = dtraffic
+        result["decode"] = d
+
+    if not args.no_prefix:
+        sp = {"workload": "cfg4 shared prefix: 128 requests over 8 prompts x 2048 tokens (BASELINE.json configs[3])"}
+        sp["decode"] = section_decode("cfg4_decode", dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_rank)
+        sp["suffix_prefill"] = section_prefill("cfg4_prefill", dev, h0, hc, args, peaks, dist_on, sampler,
+                                               seed_rank)
+        result["shared_prefix"] = sp
 
     if dist_on and not args.no_decode:
         result["decode_group_sharded"] = decode_group_sharded(dev, rank, world, args, peaks)
 
     if not args.no_decode and not args.no_loop:
-        # Decode loop (NEXT-1): consolidate once with headroom delta = 32
-        # (= max new tokens), then each step appends one token per request into its headroom,
-        # re-plans the execution domain on the host (packinfer_plan_step) and runs decode + merge.
-        import torch
-        bd = make_workload("cfg3", 0 if args.shard == "heads" else rank)
-        from synth import workloads as W
-        from paper_2602_06072_b200 import packinfer as pk
-        loop_steps, delta = 32, 32
-        tl = W.make_tensors(bd, device=dev, seed=bd.seed, extra_tokens=loop_steps)
-        rr = bd.hq // bd.hkv
-        pbl = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, rr, bd.d, torch.bfloat16, dev,
-                             headroom=delta)
-        ql = tl["q"][:, h0 * rr:(h0 + hc) * rr]
-        outl = torch.empty((bd.n, hc * rr, bd.d), dtype=torch.bfloat16, device=dev)
-        kn = torch.randn((bd.n, bd.hkv, bd.d), device=dev).to(torch.bfloat16)
-        vn = torch.randn_like(kn)
-        def loop_once():
-            pbl.replan()
-            pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0)   # consolidation
-            for k in range(1, loop_steps):
-                pbl.append(kn, vn, hkv_begin=h0)
-                pbl.replan(appended=np.full(bd.n, k, np.int32))
-                pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0, relayout=False)
-        loop_once()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        loop_once()
-        e1.record()
-        torch.cuda.synchronize()
-        lms = e0.elapsed_time(e1) / loop_steps
-        kv_tokens = sum(int(bd.kv_len.sum()) + k * bd.n for k in range(loop_steps)) / loop_steps
-        lbytes = 2 * kv_tokens * hc * bd.d * 2 + 2 * bd.n * hc * rr * bd.d * 2
-        result.setdefault("decode", {})["loop"] = {
-            "steps": loop_steps, "headroom": delta, "ms_per_step_amortized": lms,
-            "step_gbs_amortized": lbytes / (lms * 1e-3) / 1e9,
-            "note": "consolidation (relayout) once per 32 steps; per step: append + plan_step + upload + "
-                    "decode attention + merge"}
-        del tl, pbl
+        result.setdefault("decode", {})["loop"] = decode_loop(dev, h0, hc, seed_rank, args)
 
     if not args.no_mixed:
         result["mixed"] = mixed_section(dev, h0, hc, rank, args, peaks, dist_on)
 
+    result["plan"]["host_us"] = planner_us()
+
     if not args.no_e2e:
-        e_ms, h2d, d2h = e2e_steps(b, runner, max(2, min(args.steps, 10)))
+        re = Runner(b, dev, h0, hc, seed=b.seed)
+        e_ms, h2d, d2h = e2e_steps(b, re, max(3, min(args.steps, 10)))
+        del re
         if dist_on:
-            import torch.distributed as dist
-            et = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-            e_ms = float(et[0])
+            (e_ms,) = max_over_ranks(dev, e_ms)
         result["e2e"] = {"value": units_total / (e_ms * 1e-3) / 1e12,
                          "unit": "TFLOP/s", "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                          "note": "pinned host buffers; H2D of step i+1 and D2H of step i-1 overlap step i "
@@ -673,7 +967,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         f, kvb, dt, desc, cores = oracle_sample(b, args.cpu_budget, b.seed)
         result["cpu_baseline"] = {"value": f / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
-                                  "sample": desc}
+                                  "sample": desc, "planner_oracle_us": oracle_planner_us()}
+    sampler.stop()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist_on:

@@ -135,6 +135,16 @@ typedef struct {
  * (decode rows; 0 for prefill rows).                                                       */
 typedef struct { int32_t q_token, lo, hi, out; } pi_row;
 typedef struct { int32_t begin, len; } pi_span;
+/* A row segment: `count` consecutive rows [row_begin, row_begin + count) of the row table, row j
+ * of the segment being
+ *   PI_SEG_PREFILL: {q_token + j, lo, hi + j, out}   (consecutive query positions of one piece:
+ *                   the causal own-suffix gains one key per row)
+ *   PI_SEG_DECODE:  {q_token, lo, hi, out | j}       (GQA sub-head j of one decode request)
+ * The planner emits segments (O(requests + work items) host work); packinfer_plan_upload expands
+ * them into the device row table and packinfer_plan_rows into a host one.                  */
+typedef struct { int32_t row_begin, count, q_token, lo, hi, out, kind, reserved; } pi_rowseg;
+#define PI_SEG_PREFILL 0
+#define PI_SEG_DECODE 1
 /* Merge entry: output token q_token combines partial slots [slot_begin, slot_begin+count). */
 typedef struct { int32_t q_token, slot_begin, slot_count, reserved; } pi_merge;
 
@@ -148,7 +158,9 @@ typedef struct {
                                               after a suffix); copy_prefix[n_copies] == buffer_tokens */
   pi_work* prefill_work; int32_t n_prefill_work;
   pi_work* decode_work;  int32_t n_decode_work;
-  pi_row* rows;        int32_t n_rows;
+  pi_rowseg* segs;     int32_t n_segs;   /* row segments (host); the row table itself is
+                                              expanded on the device (packinfer_plan_upload)   */
+  int32_t n_rows;                          /* rows of the expanded table                      */
   pi_span* spans;      int32_t n_spans;
   pi_merge* merges;    int32_t n_merges;   int32_t n_partial_slots;
   int64_t buffer_tokens;                   /* sum of group capacities                    */
@@ -163,6 +175,8 @@ typedef struct {
   int64_t drift;         /* Eq. 4 dL = max_g L(S_g) - min_g L(S_g) including appended tokens    */
   int64_t appended_total;
   void* arena;  size_t arena_bytes;        /* the host arena holding every table          */
+  size_t rows_offset;                      /* byte offset of the row table in the DEVICE arena */
+  size_t device_arena_bytes;               /* device arena size: host tables + row table      */
 } pi_plan;
 
 /* Alg. 1 Parts 1-2 plus the packed execution domain.
@@ -193,6 +207,10 @@ PI_API pi_status packinfer_plan_step(int32_t n, const int32_t* kv_len, const int
 /* Eq. 4: 1 iff steps * drift >= capacity / 2 (inclusive, exact integer test). */
 PI_API int32_t packinfer_should_regroup(int32_t steps, int64_t drift, int32_t capacity);
 
+/* Expands the plan's row segments into rows[0 .. plan->n_rows) (host memory, caller-owned,
+ * cap >= n_rows else PI_ENOSPC): the same table packinfer_plan_upload builds on the device.   */
+PI_API pi_status packinfer_plan_rows(const pi_plan* plan, pi_row* rows, int32_t cap);
+
 /* Device view of a plan: the same tables in device memory. */
 typedef struct {
   const pi_copy* copies;  const int64_t* copy_prefix; int32_t n_copies; int64_t copy_tokens;
@@ -205,8 +223,10 @@ typedef struct {
   const int32_t* append_pos;                 /* [n_requests] (see pi_plan)                      */
 } pi_device_plan;
 
-/* Enqueue one host->device copy of plan->arena into dev_arena (device, >= plan->arena_bytes,
- * 256-byte aligned) on `stream` and fill *out with device pointers into dev_arena.        */
+/* Enqueue one host->device copy of plan->arena (arena_bytes) into dev_arena (device, >=
+ * plan->device_arena_bytes, 256-byte aligned) and one small kernel that expands the row
+ * segments into the row table at dev_arena + rows_offset, both on `stream`; fill *out with
+ * device pointers into dev_arena.                                                          */
 PI_API pi_status packinfer_plan_upload(const pi_plan* plan, void* dev_arena, size_t dev_bytes,
                                 pi_stream_t stream, pi_device_plan* out);
 

@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libpackinfer.so")
 
-SOURCES = ["capi.cpp", "plan.cpp", "device_common.cpp", "relayout.cu", "attention.cu", "merge.cu"]
+SOURCES = ["capi.cpp", "plan.cpp", "plan_device.cu", "device_common.cpp", "relayout.cu", "attention.cu", "merge.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

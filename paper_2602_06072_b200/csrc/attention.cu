@@ -42,6 +42,9 @@
 #ifndef PI_P_F16
 #define PI_P_F16 0   // experiment: P packed as fp16 against bf16 V (idesc a_fmt = f16, b_fmt = bf16)
 #endif
+#ifndef PI_P_ROUNDED_SUM
+#define PI_P_ROUNDED_SUM 1   // O normalised by the row sum of the bf16-rounded P (0: by the exact fp32 sum)
+#endif
 #ifndef PI_POLY_SAT
 #define PI_POLY_SAT 1
 #endif
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
               if constexpr (!F32) {
                 r[i] = pack_bf16(f2_lo(e), f2_hi(e));     // in place: i <= 2i
-                add_bf16x2(racc[2 * (i & 1)], racc[2 * (i & 1) + 1], r[i]);
+                if (PI_P_ROUNDED_SUM) add_bf16x2(racc[2 * (i & 1)], racc[2 * (i & 1) + 1], r[i]);
               } else {
                 r[2 * i] = __float_as_uint(f2_lo(e));
                 r[2 * i + 1] = __float_as_uint(f2_hi(e));
@@ -778,7 +781,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           }
           if (valid) {
             l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
-            lr += F32 ? (ps[0] + ps[1]) + (ps[2] + ps[3]) : (rs[0] + rs[1]) + (rs[2] + rs[3]);
+            lr += (F32 || !PI_P_ROUNDED_SUM) ? (ps[0] + ps[1]) + (ps[2] + ps[3]) : (rs[0] + rs[1]) + (rs[2] + rs[3]);
           }
         }
       }

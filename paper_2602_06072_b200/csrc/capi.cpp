@@ -80,43 +80,4 @@ int32_t packinfer_should_regroup(int32_t steps, int64_t drift, int32_t capacity)
   return (2 * (int64_t)steps * drift >= (int64_t)capacity) ? 1 : 0;
 }
 
-pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, size_t dev_bytes,
-                                pi_stream_t stream, pi_device_plan* out) {
-  if (!p || !out) return pi::fail(PI_EINVAL, "plan and out must be non-NULL");
-  if (!p->arena) return pi::fail(PI_EINVAL, "plan has no host arena (planning failed?)");
-  if (!dev_arena || dev_bytes < p->arena_bytes)
-    return pi::fail(PI_ENOSPC, "device arena too small: need " + std::to_string(p->arena_bytes));
-  if (reinterpret_cast<uintptr_t>(dev_arena) % 256)
-    return pi::fail(PI_EINVAL, "device arena must be 256-byte aligned");
-  cudaError_t e = cudaMemcpyAsync(dev_arena, p->arena, p->arena_bytes, cudaMemcpyHostToDevice,
-                                  reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return pi::fail(PI_ECUDA, std::string("plan upload: ") + cudaGetErrorString(e));
-  const char* H = static_cast<const char*>(p->arena);
-  char* D = static_cast<char*>(dev_arena);
-  auto dev = [&](const void* h) -> const void* {
-    return h ? static_cast<const void*>(D + (static_cast<const char*>(h) - H)) : nullptr;
-  };
-  std::memset(out, 0, sizeof(*out));
-  out->copies = static_cast<const pi_copy*>(dev(p->copies));
-  out->copy_prefix = static_cast<const int64_t*>(dev(p->copy_prefix));
-  out->n_copies = p->n_copies;
-  out->copy_tokens = p->copy_tokens;
-  out->prefill_work = static_cast<const pi_work*>(dev(p->prefill_work));
-  out->n_prefill_work = p->n_prefill_work;
-  out->decode_work = static_cast<const pi_work*>(dev(p->decode_work));
-  out->n_decode_work = p->n_decode_work;
-  out->rows = static_cast<const pi_row*>(dev(p->rows));
-  out->spans = static_cast<const pi_span*>(dev(p->spans));
-  out->merges = static_cast<const pi_merge*>(dev(p->merges));
-  out->n_merges = p->n_merges;
-  out->n_partial_slots = p->n_partial_slots;
-  out->append_pos = static_cast<const int32_t*>(dev(p->append_pos));
-  out->buffer_tokens = p->buffer_tokens;
-  out->n_requests = p->n_requests;
-  out->total_q = p->total_q;
-  out->gqa_ratio = p->gqa_ratio;
-  out->tile_k = 128;
-  return pi::ok();
-}
-
 }  // extern "C"

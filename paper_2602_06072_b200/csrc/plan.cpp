@@ -145,11 +145,60 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       return x.piece < y.piece;
     });
     // ---------------- Alg. 1 lines 4-9 (readings R1, R4, R6) ------------------------------
+    // Without M_max the argmin (resulting load, g) over feasible groups needs no scan: every
+    // non-holder of the piece's prefix gets load_g + len, every holder load_g + len - L_P < that,
+    // and feasibility (resulting load <= C) is monotone in the resulting load, so the answer is the
+    // best of (a) the holders (a short list per prefix) and (b) the least-loaded group overall
+    // (lowest g on ties) when it is not a holder; if that best is infeasible, none is.  A
+    // tournament tree over (load_g, g) gives (b) in O(1) and updates in O(log G): O(N log G)
+    // instead of O(N G) (cfg3: 338 pieces x 143 groups).  With M_max > 0 feasibility also depends
+    // on member counts, so the plain scan below is used.  Both are the same argmin (R1).
+    const bool fast = cfg->mem_cap == 0;
+    int32_t TS = 1;
+    while (TS < G0 + NP) TS <<= 1;
+    std::vector<int32_t> tree(fast ? 2 * TS : 0, -1);   // leaf g at TS + g; -1 = no group
+    std::vector<int64_t> tload(fast ? TS : 0, 0);
+    auto better = [&](int32_t a, int32_t b) -> int32_t {   // (load, g) lexicographic min
+      if (a < 0) return b;
+      if (b < 0) return a;
+      return (tload[b] < tload[a] || (tload[b] == tload[a] && b < a)) ? b : a;
+    };
+    auto tree_set = [&](int32_t g, int64_t load) {
+      tload[g] = load;
+      int32_t x = TS + g;
+      tree[x] = g;
+      for (x >>= 1; x >= 1; x >>= 1) tree[x] = better(tree[2 * x], tree[2 * x + 1]);
+    };
+    std::vector<std::vector<int32_t>> holders(fast ? n_prefix : 0);   // groups holding prefix p
+    if (fast) {
+      for (int32_t g = 0; g < G0; ++g) tree[TS + g] = g;
+      for (int32_t x = TS - 1; x >= 1; --x) tree[x] = better(tree[2 * x], tree[2 * x + 1]);
+    }
     for (int32_t k : order) {
       Piece& pc = pieces[k];
       int32_t best_g = -1;
       int64_t best_load = 0, best_c = 0;
-      for (int32_t g = 0; g < (int32_t)groups.size(); ++g) {
+      if (fast) {
+        const int32_t m = tree[1];
+        if (m >= 0 && !(pc.prefix >= 0 && groups[m].holds(pc.prefix))) {
+          best_g = m;
+          best_load = tload[m] + pc.kv_len;
+          best_c = pc.kv_len;
+        }
+        if (pc.prefix >= 0) {
+          const int64_t c = pc.kv_len - prefix_len[pc.prefix];
+          for (int32_t g : holders[pc.prefix]) {
+            const int64_t v = tload[g] + c;
+            if (best_g < 0 || v < best_load || (v == best_load && g < best_g)) {
+              best_g = g;
+              best_load = v;
+              best_c = c;
+            }
+          }
+        }
+        if (best_g >= 0 && best_load > C) best_g = -1;
+      }
+      for (int32_t g = 0; !fast && g < (int32_t)groups.size(); ++g) {
         const Group& grp = groups[g];
         const int64_t shared = (pc.prefix >= 0 && grp.holds(pc.prefix)) ? prefix_len[pc.prefix] : 0;
         const int64_t c = pc.kv_len - shared;
@@ -169,7 +218,11 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       Group& grp = groups[best_g];
       grp.load += best_c;
       grp.members.push_back(k);
-      if (pc.prefix >= 0 && !grp.holds(pc.prefix)) grp.held.push_back(pc.prefix);
+      if (pc.prefix >= 0 && !grp.holds(pc.prefix)) {
+        grp.held.push_back(pc.prefix);
+        if (fast) holders[pc.prefix].push_back(best_g);
+      }
+      if (fast) tree_set(best_g, grp.load);
       pc.group = best_g;
     }
   }
@@ -228,7 +281,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   std::vector<int64_t> q_off(n + 1, 0);
   for (int32_t i = 0; i < n; ++i) q_off[i + 1] = q_off[i] + q_len[i];
   std::vector<pi_work> pwork, dwork;
-  std::vector<pi_row> rows;
+  std::vector<pi_rowseg> segs;   // row segments (the per-row table is expanded on the device)
+  int32_t n_rows = 0;
   std::vector<pi_span> spans;
   auto piece_buf = [&](int32_t k) -> int64_t {  // global buffer start of a piece's suffix
     return groups[pieces[k].group].base + offsets[k].d_suffix;
@@ -236,20 +290,22 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   auto add_span = [&](int64_t b, int64_t len) { spans.push_back({(int32_t)b, (int32_t)len}); };
   int64_t valid_cells = 0, tile_cells = 0;
 
+  using Member = std::pair<int32_t, std::pair<int32_t, int32_t>>;   // piece, [a0, a1)
   struct OpenTile {
     bool open = false;
     int32_t g = -1, ctx = -1, nrows = 0;
-    std::vector<std::pair<int32_t, std::pair<int32_t, int32_t>>> members;  // piece, [a0, a1)
+    std::vector<Member> members;
   } ot;
+  ot.members.reserve(TQ);
+  segs.reserve(2 * (size_t)NP + (size_t)total_q / TQ + 16);
 
-  auto emit_tile = [&](int32_t g, int32_t ctx,
-                       const std::vector<std::pair<int32_t, std::pair<int32_t, int32_t>>>& mem) {
+  auto emit_tile = [&](int32_t g, int32_t ctx, const Member* mem, int32_t n_mem) {
     pi_work w{};
     w.kind = 0;
     w.group = g;
-    w.row_begin = (int32_t)rows.size();
+    w.row_begin = n_rows;
     w.span_begin = (int32_t)spans.size();
-    const int32_t k0 = mem.front().first;
+    const int32_t k0 = mem[0].first;
     const int32_t i0 = pieces[k0].request;
     const bool split = first_piece[i0 + 1] - first_piece[i0] > 1;
     int64_t full_keys = 0;
@@ -264,23 +320,28 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       add_span(pb, offsets[k0].l_prefix);
       full_keys += offsets[k0].l_prefix;
     }
+    // one row segment per member: rows pos = a0 .. a1-1 are (q_token0 + j, lo, hi0 + j) (the
+    // causal own-suffix grows by one key per row); the device expands them (packinfer_plan_upload)
     int64_t hull_lo = INT64_MAX, hull_hi = INT64_MIN;
-    for (const auto& m : mem) {
+    for (int32_t mi = 0; mi < n_mem; ++mi) {
+      const Member& m = mem[mi];
       const int32_t k = m.first;
       const Piece& pc = pieces[k];
       const int32_t i = pc.request;
       const int64_t lo = piece_buf(k);
       const int64_t first_pos = (int64_t)kv_len[i] - q_len[i];
-      for (int32_t pos = m.second.first; pos < m.second.second; ++pos) {
-        const int64_t hi = lo + (pos - pc.kv_begin - offsets[k].l_prefix) + 1;
-        rows.push_back({(int32_t)(q_off[i] + (pos - first_pos)), (int32_t)lo, (int32_t)hi, 0});
-        hull_lo = std::min(hull_lo, lo);
-        hull_hi = std::max(hull_hi, hi);
-        valid_cells += full_keys + (hi - lo);
-      }
+      const int64_t cnt = m.second.second - m.second.first;
+      if (cnt <= 0) continue;
+      const int64_t hi0 = lo + (m.second.first - pc.kv_begin - offsets[k].l_prefix) + 1;
+      segs.push_back({n_rows, (int32_t)cnt, (int32_t)(q_off[i] + (m.second.first - first_pos)), (int32_t)lo,
+                      (int32_t)hi0, 0, PI_SEG_PREFILL, 0});
+      n_rows += (int32_t)cnt;
+      hull_lo = std::min(hull_lo, lo);
+      hull_hi = std::max(hull_hi, hi0 + cnt - 1);
+      valid_cells += cnt * (full_keys + hi0 - lo) + cnt * (cnt - 1) / 2;
     }
     add_span(hull_lo, hull_hi - hull_lo);
-    w.row_count = (int32_t)rows.size() - w.row_begin;
+    w.row_count = n_rows - w.row_begin;
     w.span_count = (int32_t)spans.size() - w.span_begin;
     int64_t nk = 0;
     for (int32_t s = w.span_begin; s < (int32_t)spans.size(); ++s) nk += ceil_div(spans[s].len, TK);
@@ -289,7 +350,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
     pwork.push_back(w);
   };
   auto close_tile = [&]() {
-    if (ot.open && !ot.members.empty()) emit_tile(ot.g, ot.ctx, ot.members);
+    if (ot.open && !ot.members.empty()) emit_tile(ot.g, ot.ctx, ot.members.data(), (int32_t)ot.members.size());
     ot.open = false;
     ot.members.clear();
     ot.nrows = 0;
@@ -307,8 +368,10 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       const bool split = first_piece[i + 1] - first_piece[i] > 1;
       if (split || nrows >= TQ || no_qpack) {
         close_tile();
-        for (int32_t c = a0; c < a1; c += TQ)
-          emit_tile(g, e.ctx, {{e.piece, {c, std::min(a1, c + TQ)}}});
+        for (int32_t c = a0; c < a1; c += TQ) {
+          const Member one{e.piece, {c, std::min(a1, c + TQ)}};
+          emit_tile(g, e.ctx, &one, 1);
+        }
         continue;
       }
       if (!(ot.open && ot.g == g && ot.ctx == e.ctx && ot.nrows + nrows <= TQ)) {
@@ -325,47 +388,57 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
 
   // ---------------- decode work (rows = (request, GQA head); q_len == 1) -------------------
   std::vector<int32_t> dcount(n, 0);
-  std::vector<std::vector<int32_t>> item_members;  // decode requests of each decode item
-  auto emit_decode = [&](int32_t g, const std::vector<int32_t>& reqs, int64_t b, int64_t len) {
+  std::vector<int32_t> item_seg;   // first row segment of each decode item: one segment per member
+  std::vector<int32_t> dm;         // scratch: decode members of a prefix entry
+  auto emit_decode = [&](int32_t g, const int32_t* reqs, int32_t n_reqs, int64_t b, int64_t len) {
     for (int64_t c0 = 0; c0 < len; c0 += chunk) {
       const int64_t cl = std::min<int64_t>(chunk, len - c0);
       pi_work w{};
       w.kind = 1;
       w.group = g;
-      w.row_begin = (int32_t)rows.size();
+      w.row_begin = n_rows;
       w.span_begin = (int32_t)spans.size();
       add_span(b + c0, cl);
-      for (int32_t i : reqs) {
-        for (int32_t h = 0; h < r; ++h)
-          rows.push_back({(int32_t)q_off[i], (int32_t)(b + c0), (int32_t)(b + c0 + cl), h});
+      item_seg.push_back((int32_t)segs.size());
+      for (int32_t mi = 0; mi < n_reqs; ++mi) {   // r rows (request i, GQA sub-head h = 0..r-1); out set below
+        const int32_t i = reqs[mi];
+        // reserved holds the request until the slot pass below (then 0)
+        segs.push_back({n_rows, r, (int32_t)q_off[i], (int32_t)(b + c0), (int32_t)(b + c0 + cl), 0, PI_SEG_DECODE, i});
+        n_rows += r;
         dcount[i] += 1;
       }
-      w.row_count = (int32_t)rows.size() - w.row_begin;
+      w.row_count = n_rows - w.row_begin;
       w.span_count = 1;
       w.n_ktiles = (int32_t)ceil_div(cl, TK);
       dwork.push_back(w);
-      item_members.push_back(reqs);
     }
   };
   const int32_t per_block = std::max(1, TQ / r);
+  {  // upper bound of the decode items: every entry's span (plus appended keys) in chunks
+    size_t est = 0;
+    for (int32_t g = 0; g < G; ++g) est += (size_t)(groups[g].cap / chunk) + 2 * entries[g].size();
+    dwork.reserve(est);
+    item_seg.reserve(est);
+    spans.reserve(spans.size() + est);
+    segs.reserve(segs.size() + est + (size_t)n);
+  }
   for (int32_t g = 0; g < G; ++g) {
     const auto& ent = entries[g];
     for (size_t a = 0; a < ent.size(); ++a) {
       const Entry& e = ent[a];
       if (e.ctx >= 0 && e.first_of_ctx) {  // shared prefix: read once for all decode members
-        std::vector<int32_t> dm;
+        dm.clear();
         for (size_t b = a; b < ent.size() && ent[b].ctx == e.ctx; ++b)
           if (q_len[pieces[ent[b].piece].request] == 1) dm.push_back(pieces[ent[b].piece].request);
         const int64_t pb = groups[g].base + offsets[e.piece].d_prefix;
-        for (size_t s = 0; s < dm.size(); s += per_block) {
-          std::vector<int32_t> blk(dm.begin() + s, dm.begin() + std::min(dm.size(), s + per_block));
-          emit_decode(g, blk, pb, offsets[e.piece].l_prefix);
-        }
+        for (size_t s = 0; s < dm.size(); s += per_block)
+          emit_decode(g, dm.data() + s, (int32_t)(std::min(dm.size(), s + per_block) - s), pb,
+                      offsets[e.piece].l_prefix);
       }
       const Piece& pc = pieces[e.piece];
       if (q_len[pc.request] != 1) continue;
       const bool last_piece = e.piece == first_piece[pc.request + 1] - 1;
-      emit_decode(g, {pc.request}, piece_buf(e.piece), offsets[e.piece].l_suffix + (last_piece ? app(pc.request) : 0));
+      emit_decode(g, &pc.request, 1, piece_buf(e.piece), offsets[e.piece].l_suffix + (last_piece ? app(pc.request) : 0));
     }
   }
   // partial slots for rows with more than one decode item (reading R10 / Q19)
@@ -380,10 +453,12 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
     }
   }
   for (size_t w = 0; w < dwork.size(); ++w) {
-    int32_t row = dwork[w].row_begin;
-    for (int32_t i : item_members[w]) {
+    const int32_t s_end = w + 1 < dwork.size() ? item_seg[w + 1] : (int32_t)segs.size();
+    for (int32_t sg = item_seg[w]; sg < s_end; ++sg) {
+      const int32_t i = segs[sg].reserved;
+      segs[sg].reserved = 0;
       const int32_t slot = slot_base[i] >= 0 ? slot_base[i] + occ[i]++ : -1;
-      for (int32_t h = 0; h < r; ++h, ++row) rows[row].out = ((slot + 1) << 4) | h;
+      segs[sg].out = (slot + 1) << 4;   // row h of the segment: out | h
     }
   }
   // LPT order (cost descending, stable).  Prefill items are sorted by cost bucket (32 key tiles
@@ -448,11 +523,14 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const size_t o_cprefix = reserve(sizeof(int64_t) * copy_prefix.size());
   const size_t o_pwork = reserve(sizeof(pi_work) * pwork.size());
   const size_t o_dwork = reserve(sizeof(pi_work) * dwork.size());
-  const size_t o_rows = reserve(sizeof(pi_row) * rows.size());
+  const size_t o_segs = reserve(sizeof(pi_rowseg) * segs.size());
   const size_t o_spans = reserve(sizeof(pi_span) * spans.size());
   const size_t o_merges = reserve(sizeof(pi_merge) * merges.size());
   const size_t o_append = reserve(sizeof(int32_t) * std::max(n, 1));
   const size_t need = std::max<size_t>(off, 256);
+  // device arena = the host arena's tables + the expanded row table behind them
+  const size_t o_rows = need;
+  const size_t dev_need = align_up(o_rows + sizeof(pi_row) * (size_t)n_rows, 256);
 
   std::memset(out, 0, sizeof(*out));
   out->n_pieces = NP;
@@ -461,7 +539,10 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   out->n_copies = (int32_t)copies.size();
   out->n_prefill_work = (int32_t)pwork.size();
   out->n_decode_work = (int32_t)dwork.size();
-  out->n_rows = (int32_t)rows.size();
+  out->n_rows = n_rows;
+  out->n_segs = (int32_t)segs.size();
+  out->rows_offset = o_rows;
+  out->device_arena_bytes = dev_need;
   out->n_spans = (int32_t)spans.size();
   out->n_merges = (int32_t)merges.size();
   out->n_partial_slots = n_slots;
@@ -493,7 +574,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   out->copy_prefix = reinterpret_cast<int64_t*>(A + o_cprefix);
   out->prefill_work = reinterpret_cast<pi_work*>(A + o_pwork);
   out->decode_work = reinterpret_cast<pi_work*>(A + o_dwork);
-  out->rows = reinterpret_cast<pi_row*>(A + o_rows);
+  out->segs = reinterpret_cast<pi_rowseg*>(A + o_segs);
   out->spans = reinterpret_cast<pi_span*>(A + o_spans);
   out->merges = reinterpret_cast<pi_merge*>(A + o_merges);
   out->append_pos = reinterpret_cast<int32_t*>(A + o_append);
@@ -509,7 +590,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   std::memcpy(out->copy_prefix, copy_prefix.data(), sizeof(int64_t) * copy_prefix.size());
   if (!pwork.empty()) std::memcpy(out->prefill_work, pwork.data(), sizeof(pi_work) * pwork.size());
   if (!dwork.empty()) std::memcpy(out->decode_work, dwork.data(), sizeof(pi_work) * dwork.size());
-  if (!rows.empty()) std::memcpy(out->rows, rows.data(), sizeof(pi_row) * rows.size());
+  if (!segs.empty()) std::memcpy(out->segs, segs.data(), sizeof(pi_rowseg) * segs.size());
   if (!spans.empty()) std::memcpy(out->spans, spans.data(), sizeof(pi_span) * spans.size());
   if (!merges.empty()) std::memcpy(out->merges, merges.data(), sizeof(pi_merge) * merges.size());
   std::memcpy(out->append_pos, append_pos.data(), sizeof(int32_t) * std::max(n, 1));
@@ -517,3 +598,16 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
 }
 
 }  // namespace pi
+
+extern "C" pi_status packinfer_plan_rows(const pi_plan* plan, pi_row* rows, int32_t cap) {
+  if (!plan) return pi::fail(PI_EINVAL, "plan is NULL");
+  if (plan->n_rows > 0 && (!plan->segs || !rows)) return pi::fail(PI_EINVAL, "plan has no segments / rows is NULL");
+  if (cap < plan->n_rows) return pi::fail(PI_ENOSPC, "rows capacity < n_rows = " + std::to_string(plan->n_rows));
+  for (int32_t s = 0; s < plan->n_segs; ++s) {
+    const pi_rowseg& g = plan->segs[s];
+    for (int32_t j = 0; j < g.count; ++j)
+      rows[g.row_begin + j] = g.kind == PI_SEG_PREFILL ? pi_row{g.q_token + j, g.lo, g.hi + j, g.out}
+                                                       : pi_row{g.q_token, g.lo, g.hi, g.out | j};
+  }
+  return pi::ok();
+}

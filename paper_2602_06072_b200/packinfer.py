@@ -27,7 +27,7 @@ PI_BF16, PI_FP32, PI_BF16_OUT_F32 = 0, 1, 2
 
 EXPORTS = [
     "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
-    "packinfer_plan", "packinfer_plan_upload", "packinfer_relayout_kv",
+    "packinfer_plan", "packinfer_plan_rows", "packinfer_plan_upload", "packinfer_relayout_kv",
     "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_attention", "packinfer_merge",
     "packinfer_plan_step", "packinfer_should_regroup", "packinfer_append_kv",
 ]
@@ -57,6 +57,8 @@ WORK_DT = np.dtype([("kind", "<i4"), ("group", "<i4"), ("row_begin", "<i4"), ("r
                     ("span_begin", "<i4"), ("span_count", "<i4"), ("n_ktiles", "<i4"), ("reserved", "<i4")])
 ROW_DT = np.dtype([("q_token", "<i4"), ("lo", "<i4"), ("hi", "<i4"), ("out", "<i4")])
 SPAN_DT = np.dtype([("begin", "<i4"), ("len", "<i4")])
+SEG_DT = np.dtype([("row_begin", "<i4"), ("count", "<i4"), ("q_token", "<i4"), ("lo", "<i4"), ("hi", "<i4"),
+                   ("out", "<i4"), ("kind", "<i4"), ("reserved", "<i4")])
 MERGE_DT = np.dtype([("q_token", "<i4"), ("slot_begin", "<i4"), ("slot_count", "<i4"), ("reserved", "<i4")])
 
 
@@ -68,7 +70,7 @@ class pi_plan(C.Structure):
                 ("copy_prefix", C.c_void_p),
                 ("prefill_work", C.c_void_p), ("n_prefill_work", C.c_int32),
                 ("decode_work", C.c_void_p), ("n_decode_work", C.c_int32),
-                ("rows", C.c_void_p), ("n_rows", C.c_int32),
+                ("segs", C.c_void_p), ("n_segs", C.c_int32), ("n_rows", C.c_int32),
                 ("spans", C.c_void_p), ("n_spans", C.c_int32),
                 ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
                 ("buffer_tokens", C.c_int64), ("copy_tokens", C.c_int64),
@@ -78,7 +80,8 @@ class pi_plan(C.Structure):
                 ("valid_cells", C.c_int64), ("tile_cells", C.c_int64),
                 ("discrepancy", C.c_int32), ("reserved", C.c_int32),
                 ("append_pos", C.c_void_p), ("drift", C.c_int64), ("appended_total", C.c_int64),
-                ("arena", C.c_void_p), ("arena_bytes", C.c_size_t)]
+                ("arena", C.c_void_p), ("arena_bytes", C.c_size_t),
+                ("rows_offset", C.c_size_t), ("device_arena_bytes", C.c_size_t)]
 
 
 class pi_device_plan(C.Structure):
@@ -113,6 +116,8 @@ def lib():
         L.packinfer_plan.restype = C.c_int
         L.packinfer_plan.argtypes = [i32, vp, vp, vp, i32, vp, C.POINTER(pi_config), vp, C.c_size_t,
                                      C.POINTER(pi_plan)]
+        L.packinfer_plan_rows.restype = C.c_int
+        L.packinfer_plan_rows.argtypes = [C.POINTER(pi_plan), vp, i32]
         L.packinfer_plan_step.restype = C.c_int
         L.packinfer_plan_step.argtypes = [i32, vp, vp, vp, i32, vp, vp, C.POINTER(pi_config), vp, C.c_size_t,
                                           C.POINTER(pi_plan)]
@@ -182,7 +187,15 @@ class HostPlan:
     @property
     def decode_work(self): return self._view("decode_work", self.c.n_decode_work, WORK_DT)
     @property
-    def rows(self): return self._view("rows", self.c.n_rows, ROW_DT)
+    def segs(self): return self._view("segs", self.c.n_segs, SEG_DT)
+    @property
+    def rows(self):
+        """The row table, expanded on the host from the row segments (packinfer_plan_rows; the
+        device builds the same table in packinfer_plan_upload)."""
+        rows = np.zeros(int(self.c.n_rows), ROW_DT)
+        _check(lib().packinfer_plan_rows(C.byref(self.c), rows.ctypes.data if rows.size else None, rows.size),
+               "packinfer_plan_rows")
+        return rows
     @property
     def spans(self): return self._view("spans", self.c.n_spans, SPAN_DT)
     @property
@@ -353,7 +366,7 @@ class PackedBatch:
         self.device = torch.device(device)
         self.hkv, self.r, self.d, self.dtype = hkv_count, gqa_ratio, head_dim, dtype
         c = self.plan.c
-        self.dev_arena = torch.empty(max(int(c.arena_bytes), 256), dtype=torch.uint8, device=self.device)
+        self.dev_arena = torch.empty(max(int(c.device_arena_bytes), 256), dtype=torch.uint8, device=self.device)
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena)
         self._events[0] = torch.cuda.Event()
         self._events[0].record()
@@ -385,8 +398,8 @@ class PackedBatch:
         self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, arena=self._arenas[s],
                                    appended=appended)
         self._arenas[s] = self.plan.arena          # may have grown
-        if int(self.plan.c.arena_bytes) > self.dev_arena.numel():
-            self.dev_arena = torch.empty(int(self.plan.c.arena_bytes), dtype=torch.uint8, device=self.device)
+        if int(self.plan.c.device_arena_bytes) > self.dev_arena.numel():
+            self.dev_arena = torch.empty(int(self.plan.c.device_arena_bytes), dtype=torch.uint8, device=self.device)
         self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
         # appended tokens can push a decode suffix across a decode_chunk boundary: more decode items,
         # more partial slots (the kernels index partial_o / partial_lse by the plan's slot ids)

@@ -6,7 +6,7 @@ import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-VARIANTS = {"bf16P": (), "f16P_bf16V": ("PI_P_F16=1",)}
+VARIANTS = {"rounded_sum": (), "exact_sum": ("PI_P_ROUNDED_SUM=0",)}
 
 
 def child():

@@ -59,3 +59,38 @@ def test_both_arms_report_the_same_config():
     assert c == bench.arm_config(b, "group", 1)
     assert c["workload"].startswith("cfg2") and c["hq"] == 32 and c["hkv"] == 8 and c["head_dim"] == 128
     assert abs(c["algorithmic_tflop"] - 1.887367282688) < 1e-9
+
+
+def test_gpus_n_self_launches_n_ranks():
+    """bench.py --gpus 2 outside torchrun re-launches itself under torchrun with 2 ranks (dry-run
+    hook: the ranks rendezvous over gloo on 127.0.0.1 and report the world they formed)."""
+    import json
+    import subprocess
+    env = dict(os.environ, PI_BENCH_DRYRUN="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line == {"dryrun": True, "world": 2, "ranks_seen": 2, "kv_head_shards": [[0, 4], [4, 4]]}
+
+
+def test_gpus_n_without_enough_devices_fails_loudly():
+    import subprocess
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "PI_BENCH_DRYRUN", "PI_BENCH_ONE_GPU"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "only" in r.stdout
+
+
+def test_stratified_oracle_sample_covers_all_strata():
+    b = W.cfg2_prefill(0)
+    order = bench.stratified_requests(b, 0)
+    assert sorted(order) == list(range(b.n))
+    # the first 8 picks come from 8 different length strata: shortest and longest requests both appear
+    idx = np.argsort(b.kv_len, kind="stable")
+    strata = np.array_split(idx, 8)
+    first = order[:8]
+    assert sorted(next(k for k, s in enumerate(strata) if i in s) for i in first) == list(range(8))

@@ -452,3 +452,25 @@ def test_replan_grows_partials():
                               b.kv_len + k, b.q_len, b.page_size)
         H.compare(out, lse, ro, rl)
     assert int(pb.plan.c.n_partial_slots) > slots0
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4_decode", "cfg5"])
+def test_device_row_expansion_bitwise(name):
+    """packinfer_plan_upload expands the planner's row segments on the device: the device row
+    table equals the host expansion (packinfer_plan_rows) bit for bit, and every row of every
+    work item is inside its item's range."""
+    from paper_2602_06072_b200 import packinfer as pk
+    b = W.make_batch(name)
+    cfg = pk.default_config(capacity=8192, gqa_ratio=b.hq // b.hkv)
+    hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, cfg, pinned=True)
+    c = hp.c
+    arena = torch.full((int(c.device_arena_bytes),), 0xAB, dtype=torch.uint8, device="cuda")
+    pk.packinfer_plan_upload(hp, arena)
+    torch.cuda.synchronize()
+    n = int(c.n_rows)
+    dev_rows = arena[int(c.rows_offset):int(c.rows_offset) + 16 * n].cpu().numpy().view(pk.ROW_DT)
+    host_rows = hp.rows
+    assert n > 0 and dev_rows.shape == host_rows.shape
+    assert dev_rows.tobytes() == host_rows.tobytes()
+    segs = hp.segs
+    assert int(segs["count"].sum()) == n
