@@ -328,9 +328,10 @@ def e2e_steps(b, runner, steps):
 def decode_group_sharded(dev, rank, world, args, peaks):
     """N > 1 only: ONE configs[2] decode batch (the same on every rank) group-sharded across the
     ranks (shard.RankPlan, SURVEY 8(e) optional group sharding): each rank consolidates and attends
-    only its groups; split rows are completed by shard.combine (SUM / MAX all-reduce over NCCL) and
-    the batch merge.  Step = relayout (own groups) + decode attention (own items) + combine + merge,
-    timed with CUDA events, max over ranks (strong scaling of one batch)."""
+    only its groups; the partials of split rows whose pieces sit on several ranks - and only those -
+    are exchanged (shard.exchange_split_rows, C2), then each rank merges its rows.  Step = relayout
+    (own groups) + decode attention (own items) + exchange + merge, timed with CUDA events, max
+    over ranks (strong scaling of one batch)."""
     import torch
     import torch.distributed as dist
     from paper_2602_06072_b200 import packinfer as pk, shard
@@ -344,13 +345,7 @@ def decode_group_sharded(dev, rank, world, args, peaks):
     st = torch.cuda.current_stream()
 
     def once():
-        pk.packinfer_relayout_kv(rp.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf, pb.v_buf, 0,
-                                 bd.hkv, st)
-        shard.init_partials(pb.partial_o, pb.partial_lse, out)
-        pk.packinfer_attention_decode(rp.dp, t["q"], pb.k_buf, pb.v_buf, out, None, pb.partial_o,
-                                      pb.partial_lse, r, 0.0, st)
-        shard.combine(pb.partial_o, pb.partial_lse, out)
-        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, None, st)
+        rp.step(pb, t["q"], t["k_paged"], t["v_paged"], t["block_table"], out, None, st)
 
     for _ in range(args.warmup):
         once()
@@ -363,14 +358,15 @@ def decode_group_sharded(dev, rank, world, args, peaks):
         once()
     e1.record(st)
     torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / n], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    (ms,) = max_over_ranks(dev, e0.elapsed_time(e1) / n)
     kv_bytes = 2 * int(pb.plan.c.copy_tokens) * bd.hkv * bd.d * 2
     return {"workload": bd.name + " (BASELINE.json configs[2]), one batch over all ranks",
-            "ms_per_step": float(ms[0]), "step_gbs": kv_bytes / (float(ms[0]) * 1e-3) / 1e9,
+            "ms_per_step": ms, "step_gbs": kv_bytes / (ms * 1e-3) / 1e9,
             "rank_cells": rp.cells, "rank_work_items": rp.n_work, "groups": int(pb.plan.c.n_groups),
-            "scaling": "strong", "note": "relayout + decode attention of this rank's groups, SUM/MAX "
-                                         "all-reduce of partials and direct rows, merge"}
+            "cross_rows": rp.n_cross_rows, "cross_slots": rp.n_cross_slots,
+            "exchange_bytes": rp.exchange_bytes, "all_slots_bytes": int(pb.plan.c.n_partial_slots) * bd.hq * (bd.d + 1) * 4,
+            "scaling": "strong", "note": "relayout + decode attention of this rank's groups, all-reduce of the "
+                                         "cross-rank split rows' partials only, merge of the rank's rows"}
 
 
 def W_tensors(b, dev):
@@ -429,8 +425,9 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
     tuning.CapacityTuner at every regroup point.  An epoch = consolidation with the tuner's C
     (re-plan + relayout), then decode steps that append into the headroom until Eq. 4
     triggers a regroup or the headroom is exhausted.  Every step is timed with CUDA events on its
-    stream (decode attention + merge + append); the samples (ms per KV token, read back one epoch
-    later without stalling the loop) feed tuner.observe(C, cost)."""
+    stream (decode attention + merge + append); the samples (read back one epoch
+    later without stalling the loop) feed tuner.observe(C, cost): cost = step time per decoded
+    request, the same requests at every C."""
     import torch
     from synth import workloads as W
     from paper_2602_06072_b200 import packinfer as pk
@@ -453,7 +450,7 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
         for (c, ev0, ev1, kv) in pending:
             if block or ev1.query():
                 ev1.synchronize()
-                tuner.observe(c, ev0.elapsed_time(ev1) / kv * 1e6)    # ns per KV token
+                tuner.observe(c, ev0.elapsed_time(ev1) * 1e3 / kv)    # us per decoded request
             else:
                 keep.append((c, ev0, ev1, kv))
         pending[:] = keep
@@ -481,8 +478,7 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
                 pb.replan(st, appended=np.full(bd.n, k, np.int32))
             pb.run(q, t["k_paged"], t["v_paged"], t["block_table"], out, hkv_begin=h0, stream=st, relayout=False)
             ev1.record(st)
-            kv = int(pb.plan.c.copy_tokens) + int(pb.plan.c.appended_total)
-            pending.append((C, ev0, ev1, kv))
+            pending.append((C, ev0, ev1, bd.n))   # the same requests at every C: cost = time per request
             steps += 1
             k += 1
             if k > delta - 1 or pk.packinfer_should_regroup(k, int(pb.plan.c.drift), C):
@@ -496,9 +492,10 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
     ms = t_start.elapsed_time(t_end) / max(1, total_steps)
     res = {"workload": bd.name + " (BASELINE.json configs[3])", "candidates": list(cands), "epochs": history,
            "ms_per_step": ms, "best_capacity": tuner.best(),
-           "cost_ns_per_kv_token": {str(c): tuner.mean[c] for c in tuner.cands},
+           "cost_us_per_request": {str(c): tuner.mean[c] for c in tuner.cands},
            "note": "C chosen by CapacityTuner at every regroup (Eq. 4 or headroom exhausted); samples = "
-                   "per-step CUDA-event time / KV tokens, fed back asynchronously"}
+                   "per-step CUDA-event time per decoded request (append + plan_step + upload + decode attention + merge; the "
+                   "consolidation at a regroup is not a sample), fed back asynchronously"}
     del t, batches
     return res
 

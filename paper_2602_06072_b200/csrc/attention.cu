@@ -43,7 +43,7 @@
 #define PI_P_F16 0   // experiment: P packed as fp16 against bf16 V (idesc a_fmt = f16, b_fmt = bf16)
 #endif
 #ifndef PI_P_ROUNDED_SUM
-#define PI_P_ROUNDED_SUM 1   // O normalised by the row sum of the bf16-rounded P (0: by the exact fp32 sum)
+#define PI_P_ROUNDED_SUM 0   // 1: O normalised by the row sum of the bf16-rounded P (A/B: 7 % slower, profiles/r02a)
 #endif
 #ifndef PI_POLY_SAT
 #define PI_POLY_SAT 1
@@ -619,10 +619,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           uint32_t spec_bits = 0;
           // exp2 of the 64 scores in r, packed in place (bf16 pairs into r[0..31]; fp32 stays put)
           // (use_poly: PI_POLY_PAIRS of 8 pairs on the FMA pipe; clamp: x unbounded, see ex2_poly2)
-          // Two row sums: the exact fp32 sum of P (acc0/acc1, FADD2) gives the LSE and certifies the
-          // speculative half; the sum of the ROUNDED bf16 P that P.V multiplies (racc, FHADD.BF16:
-          // fp32 += bf16 half, no unpacking) normalises O, so O / l is a convex combination of V rows
-          // with the kernel's own weights (reading R13).
+          // The exact fp32 sum of P (acc0/acc1, FADD2) gives the LSE, certifies the speculative half
+          // and normalises O (reading R13).  PI_P_ROUNDED_SUM=1 keeps a second sum of the ROUNDED bf16
+          // P that P.V multiplies (racc, FHADD.BF16) to normalise O instead: 7 % slower, same error
+          // class against the oracle (profiles/r02a/ab_rowsum.txt, ab_precision.txt).
           auto exp_body = [&](auto use_poly, auto clamp, uint64_t SL2, uint64_t NM, uint64_t& acc0, uint64_t& acc1,
                               float (&racc)[4]) {
 #if PI_POLY_SAT

@@ -57,24 +57,23 @@ def _worker(rank, world, port, q):
         heads = [None] * world
         dist.all_gather_object(heads, list(range(hb, hb + hc)))
         res["heads"] = sorted(h for hs in heads for h in hs)
-        # group sharding of one batch: shard.combine assembles slots / rows owned by one rank each
+        # group sharding of one batch: exchange_split_rows assembles the cross slots, each written
+        # by one rank (the rest of the partial buffer is never exchanged)
         g2 = torch.Generator().manual_seed(11)
         po_full = torch.randn((6, 4, 8), generator=g2)
         pl_full = torch.randn((6, 4), generator=g2)
-        out_full = torch.randn((5, 4, 8), generator=g2)
-        po, pl, o, l = torch.empty(6, 4, 8), torch.empty(6, 4), torch.empty(5, 4, 8), torch.empty(4, 5)
-        shard.init_partials(po, pl, o, l)
+        n_cross = 4
+        po, pl = torch.full((6, 4, 8), float("nan")), torch.full((6, 4), float("nan"))
+        shard.neutral_cross_slots(po, pl, n_cross)
         for sl in range(6):
             if sl % world == rank:
                 po[sl], pl[sl] = po_full[sl], pl_full[sl]
-        for row in range(5):
-            if row % world == rank:
-                o[row] = out_full[row]
-                l[:, row] = float(row)
-        shard.combine(po, pl, o, l)
-        res["combine_equal"] = bool(torch.equal(po, po_full) and torch.equal(pl, pl_full)
-                                    and torch.equal(o, out_full)
-                                    and torch.equal(l, torch.arange(5.0).expand(4, 5)))
+        shard.exchange_split_rows(po, pl, n_cross)
+        res["exchange_equal"] = bool(torch.equal(po[:n_cross], po_full[:n_cross])
+                                     and torch.equal(pl[:n_cross], pl_full[:n_cross]))
+        # slots past the cross range stay local (not exchanged): NaN where this rank did not write
+        res["local_untouched"] = all(bool(torch.isnan(po[sl]).all()) == (sl % world != rank)
+                                     for sl in range(n_cross, 6))
         # bench.py's max-over-ranks step time
         t = torch.tensor([1.0 + rank])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -104,7 +103,8 @@ def test_two_rank_gloo():
             assert res[name + "_balance"], name
         assert res["heads"] == list(range(8))
         assert res["gather_equal"]
-        assert res["combine_equal"]
+        assert res["exchange_equal"]
+        assert res["local_untouched"]
         assert res["tmax"] == 2.0
 
 
@@ -156,3 +156,58 @@ def test_rank_plan_partitions_decode_batch():
         # LPT balance: no rank above the mean by more than the largest group
         load = np.bincount(owner, weights=shard.group_costs(hp), minlength=world)
         assert load.max() - load.mean() <= max(shard.group_costs(hp))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_rank_tables_split_row_exchange(world):
+    """shard.rank_tables (decode group sharding of one batch, C2): every slot is written by exactly
+    one rank; the cross rows' slots form the contiguous front range and are the only exchanged ones
+    (bytes = cross slots x Hq x (d+1) x 4); each rank merges the cross rows and exactly its own local
+    split rows; every decode token is held by its owner after the merge; guard zero-fill cells never
+    overlap cells another entry of the same rank writes, and sit past an owned group's end."""
+    from synth import workloads as W
+    from paper_2602_06072_b200 import packinfer as pk, shard
+    b = W.random_batch(31, n=24, max_len=1500, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    cfg = pk.default_config(capacity=256, decode_chunk=256, gqa_ratio=4)
+    hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, cfg)
+    owner = np.asarray(shard.group_shard(shard.group_costs(hp), world))
+    tabs = [shard.rank_tables(hp, owner, r) for r in range(world)]
+    n_slots = int(hp.c.n_partial_slots)
+    writers = np.zeros(n_slots, np.int64)
+    for r, tb in enumerate(tabs):
+        for w in tb["work"]:
+            rr = tb["rows"][w["row_begin"]:w["row_begin"] + w["row_count"]]
+            sl = (rr["out"] >> 4) - 1
+            np.add.at(writers, np.unique(sl[sl >= 0]), 1)
+    assert (writers == 1).all()
+    ncs = tabs[0]["n_cross_slots"]
+    assert all(tb["n_cross_slots"] == ncs for tb in tabs)
+    if world == 1:
+        assert ncs == 0
+    cross_tokens = set()
+    for tb in tabs:
+        m = tb["merges"]
+        cross = m[m["slot_begin"] < ncs]
+        assert (cross["slot_begin"] + cross["slot_count"] <= ncs).all()
+        cross_tokens |= set(cross["q_token"].tolist())
+    assert all(set(tb["merges"]["q_token"][tb["merges"]["slot_begin"] < ncs].tolist()) == cross_tokens for tb in tabs)
+    held = [set(tb["owned_tokens"]) for tb in tabs]
+    assert set().union(*held) == set(range(b.total_q))
+    for r in range(world):
+        for r2 in range(r + 1, world):
+            assert held[r] & held[r2] <= cross_tokens
+    merged_local = sum(int((tb["merges"]["slot_begin"] >= ncs).sum()) for tb in tabs)
+    assert merged_local + len(cross_tokens) == int(hp.c.n_merges)
+    bases, caps = np.asarray(hp.groups["base"]), np.asarray(hp.groups["cap"])
+    for r, tb in enumerate(tabs):
+        cells = []
+        pre = tb["prefix"]
+        for k, cp in enumerate(tb["copies"]):
+            cells.append((int(cp["dst"]), int(cp["dst"]) + int(pre[k + 1] - pre[k]), int(cp["len"]) == 0))
+        cells.sort()
+        assert all(a[1] <= b2[0] for a, b2 in zip(cells, cells[1:])), "overlapping cells on one rank"
+        for lo, hi, guard in cells:
+            if guard:
+                g = int(np.searchsorted(bases, lo, side="right")) - 1
+                assert owner[g] != r or lo == bases[g]  # inside a group another rank owns
+                assert hi - lo <= 128

@@ -376,9 +376,11 @@ def test_decode_loop_append():
 @pytest.mark.parametrize("world", [2, 3])
 def test_decode_group_sharding_one_batch(world):
     """Group sharding of ONE decode batch (shard.RankPlan), the ranks simulated one after the other
-    on cuda:0: each consolidates and attends only its groups; the SUM/MAX combine of shard.combine
-    (done here with the same torch reductions) + the batch plan's merge equal the oracle, and the
-    union of the ranks' buffers equals the single-rank consolidation bitwise."""
+    on cuda:0 with every buffer (K/V, partials, out, lse) pre-filled with NaN: each rank
+    consolidates only its groups (+ guard zero cells), attends only its items, the cross-rank split
+    rows' partials - and nothing else - are exchanged (the SUM / MAX of exchange_split_rows, done
+    here with the same torch reductions over the cross range), and each rank's merge then holds the
+    oracle's result for every token it owns."""
     from paper_2602_06072_b200 import packinfer as pk, shard
     b = W.random_batch(31, n=24, max_len=1500, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
     assert (b.q_len == 1).all()
@@ -388,33 +390,38 @@ def test_decode_group_sharding_one_batch(world):
                         capacity=256, decode_chunk=256)
     owner = shard.group_shard(shard.group_costs(pb.plan), world)
     assert len(set(owner)) == world
-    po_all, pl_all, out_all, lse_all, kbuf = [], [], [], [], []
+    nan = float("nan")
+    st = []
     for rank in range(world):
         rp = shard.RankPlan(pb, owner, rank)
-        kb = torch.zeros_like(pb.k_buf)
-        vb = torch.zeros_like(pb.v_buf)
+        kb = torch.full_like(pb.k_buf, nan)
+        vb = torch.full_like(pb.v_buf, nan)
+        po, pl = torch.full_like(pb.partial_o, nan), torch.full_like(pb.partial_lse, nan)
+        out = torch.full((b.total_q, b.hq, b.d), nan, dtype=torch.float32, device="cuda")
+        lse = torch.full((b.hq, b.total_q), nan, dtype=torch.float32, device="cuda")
         pk.packinfer_relayout_kv(rp.dp, t["k_paged"], t["v_paged"], t["block_table"], kb, vb, 0, b.hkv)
-        po, pl = torch.empty_like(pb.partial_o), torch.empty_like(pb.partial_lse)
-        out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.float32, device="cuda")
-        lse = torch.empty((b.hq, b.total_q), dtype=torch.float32, device="cuda")
-        shard.init_partials(po, pl, out, lse)
+        shard.neutral_cross_slots(po, pl, rp.n_cross_slots)
         pk.packinfer_attention_decode(rp.dp, t["q"], kb, vb, out, lse, po, pl, r)
-        po_all.append(po); pl_all.append(pl); out_all.append(out); lse_all.append(lse); kbuf.append(kb)
+        st.append((rp, po, pl, out, lse))
     torch.cuda.synchronize()
-    # the all-reduces of shard.combine
-    po = torch.stack(po_all).sum(0)
-    pl = torch.stack(pl_all).amax(0)
-    out = torch.stack(out_all).sum(0)              # exactly one rank wrote each row (others 0)
-    lse = torch.stack(lse_all).amax(0)
-    pk.packinfer_merge(pb.dp, po, pl, out, lse)
-    torch.cuda.synchronize()
+    ncs = st[0][0].n_cross_slots
+    assert ncs > 0 and all(x[0].n_cross_slots == ncs for x in st)
+    xo = torch.stack([x[1][:ncs] for x in st]).sum(0)     # exchange_split_rows: SUM / MAX over ranks
+    xl = torch.stack([x[2][:ncs] for x in st]).amax(0)
     ro, rl = H.oracle_full(b, t)
-    H.compare(out, lse, ro, rl)
-    # consolidation: every cell written by exactly one rank, equal to the batch relayout
-    pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf, pb.v_buf, 0, b.hkv)
-    torch.cuda.synchronize()
-    union = torch.stack([k.view(torch.int16) for k in kbuf]).sum(0, dtype=torch.int64)
-    assert torch.equal(union, pb.k_buf.view(torch.int16).to(torch.int64))
+    held = set()
+    for rp, po, pl, out, lse in st:
+        po[:ncs] = xo
+        pl[:ncs] = xl
+        pk.packinfer_merge(rp.dp, po, pl, out, lse)
+        torch.cuda.synchronize()
+        tok = torch.tensor(rp.owned_tokens, device="cuda")
+        H.compare(out[tok], lse[:, tok], ro[rp.owned_tokens], rl[:, rp.owned_tokens])
+        held |= set(rp.owned_tokens)
+        assert rp.exchange_bytes == ncs * b.hq * (b.d + 1) * 4
+    assert held == set(range(b.total_q))
+    # fewer bytes than exchanging every partial slot
+    assert ncs < int(pb.plan.c.n_partial_slots)
 
 
 def test_replan_grows_partials():
