@@ -185,15 +185,18 @@ class Runner:
         self.lse = torch.empty((hkv_count * self.r, b.total_q), dtype=torch.float32, device=device)
         self.stream = torch.cuda.current_stream()
         c = self.pbs[0].plan.c
-        # relayout + row expansion (inside the plan upload) + prefill + decode + merge
-        self.launches_per_step = 1 + (c.n_segs > 0) + (c.n_prefill_work > 0) + (c.n_decode_work > 0) + \
-            (c.n_merges > 0)
+        self.relayout = True
+        # relayout + row expansion (inside the plan upload) + one attention launch (merge inside)
+        self.launches_per_step = 1 + (c.n_segs > 0) + 1
         self.kernel_events = []
         self.step_events = []
 
     def step(self, i, time_kernel=False, t=None, out=None):
-        """One batch step on this runner's stream; t / out select another (e.g. double-buffered)
-        input set / output buffer of the same shapes."""
+        """One batch step on this runner's stream: host plan + upload (+ device row expansion),
+        relayout (unless self.relayout is False: KV resident in the group layout), then ONE
+        attention launch over every work item with the LSE merge of split rows inside it
+        (packinfer_attention_merge).  t / out select another (e.g. double-buffered) input set /
+        output buffer of the same shapes."""
         pk, torch = self.pk, self.torch
         t = self.t if t is None else t
         q = self.q if t is self.t else t["q"][:, self.hkv_begin * self.r:(self.hkv_begin + self.hkv_count) * self.r]
@@ -205,23 +208,17 @@ class Runner:
         self.events[i % 2].synchronize()            # host arena of this slot no longer read by H2D
         pb.replan(self.stream)                       # host planner + async upload
         self.events[i % 2].record(self.stream)
-        pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf,
-                                 pb.v_buf, self.hkv_begin, self.hkv_count, self.stream)
+        if self.relayout:
+            pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf,
+                                     pb.v_buf, self.hkv_begin, self.hkv_count, self.stream)
         if time_kernel:
-            e0, e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), \
-                torch.cuda.Event(enable_timing=True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
-        pk.packinfer_attention_prefill(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o,
-                                       pb.partial_lse, self.r, 0.0, self.stream)
+        pk.packinfer_attention_merge(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
+                                     pb.merge_counters, self.r, 0.0, self.stream)
         if time_kernel:
             e1.record(self.stream)
-        pk.packinfer_attention_decode(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o,
-                                      pb.partial_lse, self.r, 0.0, self.stream)
-        if time_kernel:
-            e2.record(self.stream)
-            self.kernel_events.append((e0, e1, e2))
-        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, self.lse, self.stream)
-        if time_kernel:
+            self.kernel_events.append((e0, e1))
             ee = torch.cuda.Event(enable_timing=True)
             ee.record(self.stream)
             self.step_events.append((es, ee))
@@ -233,9 +230,9 @@ class Runner:
         return {"median_ms": float(np.median(v)), "p90_ms": float(np.percentile(v, 90)), "n": int(v.size)}
 
     def kernel_ms(self):
-        pre = [a.elapsed_time(b) for a, b, _ in self.kernel_events]
-        dec = [b.elapsed_time(c) for _, b, c in self.kernel_events]
-        return (sum(pre) / len(pre) if pre else 0.0), (sum(dec) / len(dec) if dec else 0.0)
+        """Average time of the step's attention launch (prefill + decode items + in-kernel merge)."""
+        v = [a.elapsed_time(b) for a, b in self.kernel_events]
+        return sum(v) / len(v) if v else 0.0
 
 
 def timed_steps(runner, steps, warmup, dist_on, window=None):
@@ -503,8 +500,8 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
 def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
     """BASELINE.json configs[4]: Llama-3-70B-shaped mixed batch (2 x 128k-token prefills split
     across groups + 30 short prefills + 224 decodes up to 32k), ONE fused attention launch over
-    prefill and decode work items (NEXT-3) + LSE merge; the split form (one launch per kind) is
-    timed beside it on the same plan."""
+    prefill and decode work items with the LSE merge inside it (NEXT-3); the split form (prefill
+    launch, decode launch, merge launch) is timed beside it on the same plan."""
     import torch
     from synth import workloads as W
     from paper_2602_06072_b200 import packinfer as pk
@@ -525,17 +522,18 @@ def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
         a, m, e = ev(), ev(), ev()
         a.record(st)
         if fused:
-            pk.packinfer_attention(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o, pbm.partial_lse,
-                                   r, 0.0, st)
+            pk.packinfer_attention_merge(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o,
+                                         pbm.partial_lse, pbm.merge_counters, r, 0.0, st)
             m.record(st)
+            e.record(st)
         else:
             pk.packinfer_attention_prefill(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o,
                                            pbm.partial_lse, r, 0.0, st)
             m.record(st)
             pk.packinfer_attention_decode(pbm.dp, qm, pbm.k_buf, pbm.v_buf, outm, lsem, pbm.partial_o,
                                           pbm.partial_lse, r, 0.0, st)
-        e.record(st)
-        pk.packinfer_merge(pbm.dp, pbm.partial_o, pbm.partial_lse, outm, lsem, st)
+            pk.packinfer_merge(pbm.dp, pbm.partial_o, pbm.partial_lse, outm, lsem, st)
+            e.record(st)
         times.append((a, m, e))
 
     steps = 2
@@ -566,8 +564,8 @@ def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
            "fused_attention_ms": fused_ms, "split_attention_ms": split_ms, "split_prefill_ms": split_pre_ms,
            "tflops_fused": flops / (fused_ms * 1e-3) / 1e12,
            "frac_fused": flops / (fused_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-           "note": "tflops_fused counts prefill FLOPs only over the fused (prefill + decode) kernel time",
-           "gpu_launches": 4 * steps}
+           "note": "tflops_fused counts prefill FLOPs only over the fused (prefill + decode + merge) kernel time",
+           "gpu_launches": 3 * steps}
     del tm, pbm
     return out
 
@@ -734,17 +732,28 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
     steps = max(10, args.steps)
     win = []
     dms = timed_steps(rd, steps, args.warmup, dist_on, win) / steps
-    _, dec_ms = rd.kernel_ms()
+    dec_ms = rd.kernel_ms()
     if dist_on:
         dms, dec_ms = max_over_ranks(dev, dms, dec_ms)
     ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
+    # KV resident in the group layout (the producer writes new tokens there, packinfer_append_kv):
+    # the step is host plan + upload + ONE attention launch with the merge inside - no relayout
+    rd.relayout = False
+    rms = timed_steps(rd, steps, args.warmup, dist_on) / steps
+    rk = rd.kernel_ms()
+    if dist_on:
+        rms, rk = max_over_ranks(dev, rms, rk)
     c = rd.pbs[0].plan.c
     out = {"ms_per_step": dms, "kernel_ms": dec_ms, "kv_bytes": kvb, "qo_bytes": qob, "achieved_gbs": ach,
            "peak_gbs": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
            "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9, "work_items": int(c.n_decode_work),
            "partial_slots": int(c.n_partial_slots), "groups": int(c.n_groups),
            "step_latency": rd.step_latency(), "gpu_launches": rd.launches_per_step * steps,
-           "clocks": sampler.window(*win) if win else None}
+           "clocks": sampler.window(*win) if win else None,
+           "resident": {"ms_per_step": rms, "kernel_ms": rk, "step_over_kernel": rms / rk,
+                        "step_gbs": (kvb + qob) / (rms * 1e-3) / 1e9, "gpu_launches_per_step": 2,
+                        "note": "KV resident in the group-contiguous layout: plan + upload (+ row expansion) "
+                                "+ one attention launch with the in-kernel merge; no relayout"}}
     del rd
     return out
 
@@ -758,7 +767,7 @@ def section_prefill(name, dev, h0, hc, args, peaks, dist_on, sampler, seed_rank)
     steps = max(10, args.steps)
     win = []
     pms = timed_steps(rp, steps, args.warmup, dist_on, win) / steps
-    pre_ms, _ = rp.kernel_ms()
+    pre_ms = rp.kernel_ms()
     if dist_on:
         pms, pre_ms = max_over_ranks(dev, pms, pre_ms)
     ach = flops / (pre_ms * 1e-3) / 1e12
@@ -847,7 +856,7 @@ def main():
     total_ms = timed_steps(runner, args.steps, args.warmup, dist_on, win)
     clocks = sampler.window(*win)
     ms_step = total_ms / args.steps
-    pre_ms, _ = runner.kernel_ms()
+    pre_ms = runner.kernel_ms()
     units_total = flops
     if dist_on:
         import torch.distributed as dist

@@ -163,6 +163,7 @@ typedef struct {
   int32_t n_rows;                          /* rows of the expanded table                      */
   pi_span* spans;      int32_t n_spans;
   pi_merge* merges;    int32_t n_merges;   int32_t n_partial_slots;
+  int32_t* slot_merge;                     /* [n_partial_slots] merge entry of each slot   */
   int64_t buffer_tokens;                   /* sum of group capacities                    */
   int64_t copy_tokens;                     /* Eq. 5 volume = sum of loads                */
   int32_t n_requests, n_prefix, total_q, gqa_ratio;
@@ -221,6 +222,8 @@ typedef struct {
   int64_t buffer_tokens;
   int32_t n_requests, total_q, gqa_ratio, tile_k;
   const int32_t* append_pos;                 /* [n_requests] (see pi_plan)                      */
+  const int32_t* slot_merge;                 /* [n_partial_slots] (see pi_plan); NULL disables
+                                                packinfer_attention_merge                        */
 } pi_device_plan;
 
 /* Enqueue one host->device copy of plan->arena (arena_bytes) into dev_arena (device, >=
@@ -289,6 +292,21 @@ PI_API pi_status packinfer_attention(const pi_device_plan* dp, const void* q, in
                                      int32_t gqa_ratio, int32_t head_dim, float softmax_scale,
                                      pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
                                      float* partial_o, float* partial_lse, pi_stream_t stream);
+
+/* Fully fused form (NEXT-3; "reducing ... kernel launch overhead"): as
+ * packinfer_attention, and the LSE merge of split rows happens inside the same launch - the CTA
+ * that writes the LAST partial of a (split row, head) merges it (last-arriver epilogue: partials
+ * fenced, then one atomic per (row, head) on merge_counters), with packinfer_merge's arithmetic in
+ * the same order (outputs bitwise equal to packinfer_attention + packinfer_merge).
+ * merge_counters: device uint32 [n_merges * hkv_count * gqa_ratio], all ZERO on entry (e.g. one
+ * cudaMemset at allocation); the kernel leaves them zero when it completes.  partial_o /
+ * partial_lse are still written (the merge reads them back).                                  */
+PI_API pi_status packinfer_attention_merge(const pi_device_plan* dp, const void* q, int64_t q_row_stride,
+                                           const void* k_buf, const void* v_buf, int32_t hkv_count,
+                                           int32_t gqa_ratio, int32_t head_dim, float softmax_scale,
+                                           pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
+                                           float* partial_o, float* partial_lse, uint32_t* merge_counters,
+                                           pi_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
  * Lossless LSE merge of split rows (reading R10):

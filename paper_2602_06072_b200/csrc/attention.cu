@@ -82,6 +82,10 @@ struct AttnParams {
   unsigned long long* trace;  // debug only (packinfer_debug_trace): CTA-0 clock64 timeline
   int32_t q_heads_stride;  // q_row_stride / head_dim: rows of the 2D (token*stride + head, d) Q view
   int32_t tiles_per_unit;  // prefill: 2 (GQA head pairs; bf16) or 1 (fp32 operands)
+  // in-kernel LSE merge (packinfer_attention_merge; NULL merge_ctr = separate packinfer_merge)
+  const pi_merge* merges;
+  const int32_t* slot_merge;
+  uint32_t* merge_ctr;     // [n_merges * hq_count], zero on entry and on exit
 };
 
 // Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
@@ -117,7 +121,8 @@ struct AttnCfg {
   static constexpr int OFF_V = OFF_K + NS * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
   static constexpr int OFF_XCH = OFF_BAR + 256;       // single units: (m, l, l_rounded) of both warpgroups
-  static constexpr int SMEM = OFF_XCH + 2 * 128 * 16 + 1024;  // + alignment slack
+  static constexpr int OFF_FLAG = OFF_XCH + 2 * 128 * 16;   // single units: merge entry to finish per row
+  static constexpr int SMEM = OFF_FLAG + 128 * 4 + 1024;    // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
   // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
   static constexpr uint32_t P1_SINGLE = F32 ? 64u : 96u;
@@ -869,14 +874,85 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           }
         }
       }
-      tc_fence_before();
-      if (!u.has_b) named_bar_sync(1, 256);   // both warpgroups are done with O_0, O_1 and xch
-      mbar_arrive(&bar[B_OFREE0 + X]);
       if (valid && (u.has_b || X == 0)) {
         if (slot < 0) {
           if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
         } else {
           p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
+        }
+      }
+      // in-kernel LSE merge (last arriver): this row's partial (both column halves + lse) is made
+      // visible device-wide before ONE atomic per (split row, head); the CTA completing the count
+      // merges every slot of the row with packinfer_merge's arithmetic and order (reading R10) and
+      // re-zeroes the counter for the next launch
+      const bool fused_merge = !u.has_b && p.merge_ctr != nullptr;
+      const bool part = valid && slot >= 0;
+      if (fused_merge && part) __threadfence();
+      tc_fence_before();
+      if (!u.has_b) named_bar_sync(1, 256);   // both warpgroups are done with O_0, O_1 and xch
+      mbar_arrive(&bar[B_OFREE0 + X]);
+      if (fused_merge) {
+        int* flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
+        if (X == 0) {
+          int mm = -1;
+          if (part) {
+            const int m = p.slot_merge[slot];
+            uint32_t* ctr = p.merge_ctr + (int64_t)m * p.hq_count + head;
+            const uint32_t old = atomicAdd(ctr, 1u);
+            if (old + 1u == (uint32_t)p.merges[m].slot_count) {
+              *ctr = 0u;
+              __threadfence();
+              mm = m;
+            }
+          }
+          flag[row_id] = mm;
+        }
+        named_bar_sync(1, 256);
+        const int mm = flag[row_id];
+        if (part && mm >= 0) {
+          const pi_merge mg = p.merges[mm];
+          float M = NEG_INF;
+          for (int bb = 0; bb < mg.slot_count; ++bb)
+            M = fmaxf(M, __ldcg(&p.partial_lse[(int64_t)(mg.slot_begin + bb) * p.hq_count + head]));
+          constexpr int HD = D / 2;   // warpgroup X merges columns [X HD, (X + 1) HD)
+          float acc[HD];
+#pragma unroll
+          for (int i = 0; i < HD; ++i) acc[i] = 0.f;
+          float W = 0.f;
+          if (M != NEG_INF) {
+            for (int bb = 0; bb < mg.slot_count; ++bb) {
+              const int64_t sl = mg.slot_begin + bb;
+              const float w = expf(__ldcg(&p.partial_lse[sl * p.hq_count + head]) - M);
+              W += w;
+              const float4* src = reinterpret_cast<const float4*>(p.partial_o + (sl * p.hq_count + head) * D + X * HD);
+#pragma unroll
+              for (int v = 0; v < HD / 4; ++v) {
+                const float4 x = __ldcg(src + v);
+                acc[4 * v] += w * x.x;
+                acc[4 * v + 1] += w * x.y;
+                acc[4 * v + 2] += w * x.z;
+                acc[4 * v + 3] += w * x.w;
+              }
+            }
+          }
+          const float inv = W > 0.f ? 1.f / W : 0.f;
+          if (F32 || p.out_f32) {
+            float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)mg.q_token * p.out_row_stride + (int64_t)head * D +
+                                                             X * HD) * 4);
+#pragma unroll
+            for (int v = 0; v < HD / 4; ++v)
+              dst[v] = make_float4(acc[4 * v] * inv, acc[4 * v + 1] * inv, acc[4 * v + 2] * inv, acc[4 * v + 3] * inv);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(p.out + ((int64_t)mg.q_token * p.out_row_stride + (int64_t)head * D +
+                                                           X * HD) * 2);
+#pragma unroll
+            for (int v = 0; v < HD / 8; ++v)
+              dst[v] = make_uint4(pack_bf16(acc[8 * v] * inv, acc[8 * v + 1] * inv),
+                                  pack_bf16(acc[8 * v + 2] * inv, acc[8 * v + 3] * inv),
+                                  pack_bf16(acc[8 * v + 4] * inv, acc[8 * v + 5] * inv),
+                                  pack_bf16(acc[8 * v + 6] * inv, acc[8 * v + 7] * inv));
+          }
+          if (X == 0 && p.lse) p.lse[(int64_t)head * p.total_q + mg.q_token] = W > 0.f ? M + logf(W) : NEG_INF;
         }
       }
       if (u.has_b) {
@@ -908,7 +984,7 @@ template <int D, bool F32>
 static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const void* q, int64_t q_row_stride,
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
-                        cudaStream_t stream) {
+                        uint32_t* merge_ctr, cudaStream_t stream) {
   using C = AttnCfg<D, F32>;
   AttnParams p{};
   p.work_p = dp->prefill_work;
@@ -938,6 +1014,9 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   p.out_f32 = out_f32 ? 1 : 0;
   p.buffer_tokens = dp->buffer_tokens;
   p.trace = g_debug_trace;
+  p.merges = dp->merges;
+  p.slot_merge = dp->slot_merge;
+  p.merge_ctr = (dp->n_merges > 0 && (mode & 2)) ? merge_ctr : nullptr;
 
   CUtensorMap tmK, tmV;
   const CUtensorMapDataType dt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -970,7 +1049,7 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
                                  const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,
                                  int32_t head_dim, float softmax_scale, pi_dtype dt, void* out,
                                  int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
-                                 pi_stream_t stream) {
+                                 pi_stream_t stream, uint32_t* merge_ctr = nullptr, bool want_merge = false) {
   if (!dp) return fail(PI_EINVAL, "device plan is NULL");
   const bool decode = (mode & 2) && dp->n_decode_work > 0;
   const int32_t n_work = ((mode & 1) ? dp->n_prefill_work : 0) + ((mode & 2) ? dp->n_decode_work : 0);
@@ -991,6 +1070,8 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
     return fail(PI_EINVAL, "row stride smaller than the local heads");
   if (dp->n_partial_slots > 0 && decode && (!partial_o || !partial_lse))
     return fail(PI_EINVAL, "plan has split rows: partial_o / partial_lse required");
+  if (want_merge && decode && dp->n_merges > 0 && (!merge_ctr || !dp->slot_merge))
+    return fail(PI_EINVAL, "in-kernel merge needs merge_counters and a plan with a slot->merge table");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(k_buf) |
        reinterpret_cast<uintptr_t>(v_buf)) % 16)
     return fail(PI_EINVAL, "q/out/k_buf/v_buf must be 16-byte aligned");
@@ -1000,13 +1081,13 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dt == PI_BF16 && head_dim == 128)
     s = launch<128, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                           out_row_stride, lse, partial_o, partial_lse, st);
+                           out_row_stride, lse, partial_o, partial_lse, merge_ctr, st);
   else if (dt == PI_BF16 && head_dim == 64)
     s = launch<64, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                          out_row_stride, lse, partial_o, partial_lse, st);
+                          out_row_stride, lse, partial_o, partial_lse, merge_ctr, st);
   else
     s = launch<64, true>(dp, mode, false, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                         out_row_stride, lse, partial_o, partial_lse, st);
+                         out_row_stride, lse, partial_o, partial_lse, merge_ctr, st);
   return s == PI_OK ? ok() : s;
 }
 
@@ -1042,6 +1123,15 @@ pi_status packinfer_attention(const pi_device_plan* dp, const void* q, int64_t q
                               float* partial_o, float* partial_lse, pi_stream_t stream) {
   return pi::attention_entry(3, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim, softmax_scale,
                              dt, out, out_row_stride, lse, partial_o, partial_lse, stream);
+}
+
+pi_status packinfer_attention_merge(const pi_device_plan* dp, const void* q, int64_t q_row_stride, const void* k_buf,
+                                    const void* v_buf, int32_t hkv_count, int32_t gqa_ratio, int32_t head_dim,
+                                    float softmax_scale, pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
+                                    float* partial_o, float* partial_lse, uint32_t* merge_counters,
+                                    pi_stream_t stream) {
+  return pi::attention_entry(3, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim, softmax_scale,
+                             dt, out, out_row_stride, lse, partial_o, partial_lse, stream, merge_counters, true);
 }
 
 }  // extern "C"

@@ -526,6 +526,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const size_t o_segs = reserve(sizeof(pi_rowseg) * segs.size());
   const size_t o_spans = reserve(sizeof(pi_span) * spans.size());
   const size_t o_merges = reserve(sizeof(pi_merge) * merges.size());
+  const size_t o_slot_merge = reserve(sizeof(int32_t) * (size_t)n_slots);
   const size_t o_append = reserve(sizeof(int32_t) * std::max(n, 1));
   const size_t need = std::max<size_t>(off, 256);
   // device arena = the host arena's tables + the expanded row table behind them
@@ -577,6 +578,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   out->segs = reinterpret_cast<pi_rowseg*>(A + o_segs);
   out->spans = reinterpret_cast<pi_span*>(A + o_spans);
   out->merges = reinterpret_cast<pi_merge*>(A + o_merges);
+  out->slot_merge = reinterpret_cast<int32_t*>(A + o_slot_merge);
   out->append_pos = reinterpret_cast<int32_t*>(A + o_append);
   for (int32_t k = 0; k < NP; ++k) {
     const Piece& pc = pieces[k];
@@ -593,6 +595,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   if (!segs.empty()) std::memcpy(out->segs, segs.data(), sizeof(pi_rowseg) * segs.size());
   if (!spans.empty()) std::memcpy(out->spans, spans.data(), sizeof(pi_span) * spans.size());
   if (!merges.empty()) std::memcpy(out->merges, merges.data(), sizeof(pi_merge) * merges.size());
+  for (int32_t m = 0; m < (int32_t)merges.size(); ++m)   // slot -> its merge entry (in-kernel merge)
+    for (int32_t b = 0; b < merges[m].slot_count; ++b) out->slot_merge[merges[m].slot_begin + b] = m;
   std::memcpy(out->append_pos, append_pos.data(), sizeof(int32_t) * std::max(n, 1));
   return PI_OK;
 }

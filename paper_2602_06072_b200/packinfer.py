@@ -28,7 +28,8 @@ PI_BF16, PI_FP32, PI_BF16_OUT_F32 = 0, 1, 2
 EXPORTS = [
     "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
     "packinfer_plan", "packinfer_plan_rows", "packinfer_plan_upload", "packinfer_relayout_kv",
-    "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_attention", "packinfer_merge",
+    "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_attention", "packinfer_attention_merge",
+    "packinfer_merge",
     "packinfer_plan_step", "packinfer_should_regroup", "packinfer_append_kv",
 ]
 
@@ -73,6 +74,7 @@ class pi_plan(C.Structure):
                 ("segs", C.c_void_p), ("n_segs", C.c_int32), ("n_rows", C.c_int32),
                 ("spans", C.c_void_p), ("n_spans", C.c_int32),
                 ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
+                ("slot_merge", C.c_void_p),
                 ("buffer_tokens", C.c_int64), ("copy_tokens", C.c_int64),
                 ("n_requests", C.c_int32), ("n_prefix", C.c_int32), ("total_q", C.c_int32),
                 ("gqa_ratio", C.c_int32),
@@ -93,7 +95,7 @@ class pi_device_plan(C.Structure):
                 ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
                 ("buffer_tokens", C.c_int64),
                 ("n_requests", C.c_int32), ("total_q", C.c_int32), ("gqa_ratio", C.c_int32),
-                ("tile_k", C.c_int32), ("append_pos", C.c_void_p)]
+                ("tile_k", C.c_int32), ("append_pos", C.c_void_p), ("slot_merge", C.c_void_p)]
 
 
 _lib = None
@@ -135,6 +137,9 @@ def lib():
             f.restype = C.c_int
             f.argtypes = [C.POINTER(pi_device_plan), vp, i64, vp, vp, i32, i32, i32, f32, C.c_int, vp, i64, vp,
                           vp, vp, vp]
+        L.packinfer_attention_merge.restype = C.c_int
+        L.packinfer_attention_merge.argtypes = [C.POINTER(pi_device_plan), vp, i64, vp, vp, i32, i32, i32, f32, C.c_int,
+                                                vp, i64, vp, vp, vp, vp, vp]
         L.packinfer_merge.restype = C.c_int
         L.packinfer_merge.argtypes = [C.POINTER(pi_device_plan), vp, vp, i32, i32, C.c_int, vp, i64, vp, vp]
         _lib = L
@@ -321,6 +326,24 @@ def packinfer_attention(dp, q, k_buf, v_buf, out, lse=None, partial_o=None, part
                partial_o, partial_lse, gqa_ratio, scale, stream)
 
 
+def packinfer_attention_merge(dp, q, k_buf, v_buf, out, lse, partial_o, partial_lse, merge_counters,
+                              gqa_ratio: int = 1, scale: float = 0.0, stream=None):
+    """Fully fused (include/packinfer.h): one launch over prefill + decode work items with the LSE
+    merge of split rows inside it (last arriver); merge_counters: int32 zeros [n_merges * Hq_local]."""
+    import torch
+    hkv_count, _, d = k_buf.shape
+    dt = _dt(q)
+    if dt == PI_BF16 and out.dtype == torch.float32:
+        dt = PI_BF16_OUT_F32
+    _check(lib().packinfer_attention_merge(C.byref(dp), q.data_ptr(), q.stride(0), k_buf.data_ptr(), v_buf.data_ptr(),
+                                           hkv_count, gqa_ratio, d, float(scale), dt, out.data_ptr(), out.stride(0),
+                                           None if lse is None else lse.data_ptr(),
+                                           None if partial_o is None else partial_o.data_ptr(),
+                                           None if partial_lse is None else partial_lse.data_ptr(),
+                                           None if merge_counters is None else merge_counters.data_ptr(),
+                                           _stream_ptr(stream)), "packinfer_attention_merge")
+
+
 def packinfer_should_regroup(steps: int, drift: int, capacity: int) -> bool:
     """Eq. 4 (P:278): t * dL >= C / 2."""
     return bool(lib().packinfer_should_regroup(int(steps), int(drift), int(capacity)))
@@ -380,10 +403,14 @@ class PackedBatch:
         """partial_o / partial_lse hold at least the current plan's n_partial_slots rows."""
         import torch
         ns = max(int(self.plan.c.n_partial_slots), 1)
+        hq = self.hkv * self.r
         if self.partial_o is None or self.partial_o.shape[0] < ns:
-            hq = self.hkv * self.r
             self.partial_o = torch.empty((ns, hq, self.d), dtype=torch.float32, device=self.device)
             self.partial_lse = torch.empty((ns, hq), dtype=torch.float32, device=self.device)
+        nm = max(int(self.plan.c.n_merges), 1) * hq
+        if getattr(self, "merge_counters", None) is None or self.merge_counters.numel() < nm:
+            # zero once; the in-kernel merge leaves them zero after every launch
+            self.merge_counters = torch.zeros(nm, dtype=torch.int32, device=self.device)
 
     def replan(self, stream=None, appended=None):
         """Host planning + plan upload (the per-step host part of the hot path).  `appended`:
@@ -413,12 +440,20 @@ class PackedBatch:
         packinfer_append_kv(self.dp, k_new, v_new, self.k_buf, self.v_buf, hkv_begin, self.hkv, stream)
 
     def run(self, q, k_paged, v_paged, block_table, out, lse=None, hkv_begin: int = 0, stream=None,
-            relayout: bool = True, fused: bool = True):
+            relayout: bool = True, fused: bool = True, kernel_merge: Optional[bool] = None):
         """relayout -> attention -> merge.  fused: ONE attention launch over prefill and decode work
-        items (packinfer_attention); else one launch per kind (prefill, then decode)."""
+        items (packinfer_attention); else one launch per kind (prefill, then decode).  kernel_merge
+        (default: = fused): the LSE merge of split rows inside that launch
+        (packinfer_attention_merge) instead of a packinfer_merge launch."""
         if relayout:
             packinfer_relayout_kv(self.dp, k_paged, v_paged, block_table, self.k_buf, self.v_buf,
                                   hkv_begin, self.hkv, stream)
+        if kernel_merge is None:
+            kernel_merge = fused
+        if fused and kernel_merge:
+            packinfer_attention_merge(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
+                                      self.partial_lse, self.merge_counters, self.r, 0.0, stream)
+            return
         if fused:
             packinfer_attention(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
                                 self.partial_lse, self.r, 0.0, stream)

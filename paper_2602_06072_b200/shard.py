@@ -215,6 +215,7 @@ class RankPlan:
         dp.rows = self.rows.data_ptr()
         dp.merges = self.merges.data_ptr()
         dp.n_merges = len(tb["merges"])
+        dp.slot_merge = None                         # slots are renumbered: merge after the exchange
         dp.buffer_tokens = int(c.buffer_tokens)      # batch coordinates (dst is absolute)
         self.dp = dp
         self.n_cross_slots = tb["n_cross_slots"]

@@ -481,3 +481,37 @@ def test_device_row_expansion_bitwise(name):
     assert dev_rows.tobytes() == host_rows.tobytes()
     segs = hp.segs
     assert int(segs["count"].sum()) == n
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_in_kernel_merge_bitwise(seed):
+    """NEXT-3 last-arriver merge: packinfer_attention_merge (prefill + decode + LSE merge in ONE
+    launch) equals packinfer_attention + packinfer_merge bit for bit (same arithmetic, same slot
+    order), passes the oracle gate, and leaves every merge counter at zero (so the next launch
+    starts clean); run twice to show the counters are reusable."""
+    from paper_2602_06072_b200 import packinfer as pk
+    rng = np.random.default_rng(seed)
+    b = W.random_batch(400 + seed, n=int(rng.integers(6, 16)), max_len=int(rng.integers(600, 1800)), hq=8, hkv=2,
+                       d=128, n_prefix=2, decode_frac=0.6)
+    t = W.make_tensors(b, device="cuda")
+    r = b.hq // b.hkv
+    pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16, "cuda",
+                        capacity=512, decode_chunk=128)
+    assert int(pb.plan.c.n_merges) > 0
+    res = {}
+    for mode in ("separate", "kernel", "kernel2"):
+        for odt in (torch.float32, torch.bfloat16):
+            out = torch.full((b.total_q, b.hq, b.d), float("nan"), dtype=odt, device="cuda")
+            lse = torch.full((b.hq, b.total_q), float("nan"), dtype=torch.float32, device="cuda")
+            pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out, lse, kernel_merge=(mode != "separate"))
+            torch.cuda.synchronize()
+            res[mode, odt] = (out, lse)
+            assert int(pb.merge_counters.abs().sum()) == 0
+    for odt in (torch.float32, torch.bfloat16):
+        o0, l0 = res["separate", odt]
+        for mode in ("kernel", "kernel2"):
+            o1, l1 = res[mode, odt]
+            assert torch.equal(o0.view(torch.int8), o1.view(torch.int8)), mode
+            assert torch.equal(l0, l1)
+    ro, rl = H.oracle_full(b, t)
+    H.compare(*res["kernel", torch.float32], ro, rl)
