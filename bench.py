@@ -151,6 +151,9 @@ def algorithmic(b, plan_c, hkv_local):
 
 
 METRIC = "packed prefill TFLOP/s (cfg2 batch step)"
+# the step's attention: one launch + the packinfer_merge launch (default, measured fastest:
+# profiles/r02b/ab_merge.txt), or PI_BENCH_SEPARATE_MERGE=0 for packinfer_attention_merge (merge in-kernel)
+SEPARATE_MERGE = os.environ.get("PI_BENCH_SEPARATE_MERGE", "1") == "1"
 
 
 def arm_config(b, shard, world):
@@ -186,17 +189,18 @@ class Runner:
         self.stream = torch.cuda.current_stream()
         c = self.pbs[0].plan.c
         self.relayout = True
-        # relayout + row expansion (inside the plan upload) + one attention launch (merge inside)
-        self.launches_per_step = 1 + (c.n_segs > 0) + 1
+        # relayout + row expansion (inside the plan upload) + one attention launch + merge
+        self.launches_per_step = 1 + (c.n_segs > 0) + 1 + (SEPARATE_MERGE and c.n_merges > 0)
         self.kernel_events = []
         self.step_events = []
 
     def step(self, i, time_kernel=False, t=None, out=None):
         """One batch step on this runner's stream: host plan + upload (+ device row expansion),
         relayout (unless self.relayout is False: KV resident in the group layout), then ONE
-        attention launch over every work item with the LSE merge of split rows inside it
-        (packinfer_attention_merge).  t / out select another (e.g. double-buffered) input set /
-        output buffer of the same shapes."""
+        attention launch over every work item (packinfer_attention) and the LSE merge of split rows
+        (packinfer_merge; or in-kernel with packinfer_attention_merge, see SEPARATE_MERGE).
+        t / out select another (e.g. double-buffered) input set / output buffer of the same
+        shapes."""
         pk, torch = self.pk, self.torch
         t = self.t if t is None else t
         q = self.q if t is self.t else t["q"][:, self.hkv_begin * self.r:(self.hkv_begin + self.hkv_count) * self.r]
@@ -214,8 +218,13 @@ class Runner:
         if time_kernel:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
-        pk.packinfer_attention_merge(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
-                                     pb.merge_counters, self.r, 0.0, self.stream)
+        if SEPARATE_MERGE:   # A/B hook: attention launch + packinfer_merge launch
+            pk.packinfer_attention(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
+                                   self.r, 0.0, self.stream)
+            pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, self.lse, self.stream)
+        else:
+            pk.packinfer_attention_merge(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
+                                         pb.merge_counters, self.r, 0.0, self.stream)
         if time_kernel:
             e1.record(self.stream)
             self.kernel_events.append((e0, e1))
@@ -751,9 +760,10 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
            "step_latency": rd.step_latency(), "gpu_launches": rd.launches_per_step * steps,
            "clocks": sampler.window(*win) if win else None,
            "resident": {"ms_per_step": rms, "kernel_ms": rk, "step_over_kernel": rms / rk,
-                        "step_gbs": (kvb + qob) / (rms * 1e-3) / 1e9, "gpu_launches_per_step": 2,
+                        "step_gbs": (kvb + qob) / (rms * 1e-3) / 1e9,
+                        "gpu_launches_per_step": rd.launches_per_step - 1,
                         "note": "KV resident in the group-contiguous layout: plan + upload (+ row expansion) "
-                                "+ one attention launch with the in-kernel merge; no relayout"}}
+                                "+ one attention launch + merge; no relayout"}}
     del rd
     return out
 

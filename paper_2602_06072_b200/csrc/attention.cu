@@ -35,6 +35,8 @@
 #include <cstdint>
 #include <type_traits>
 
+#include <cuda_bf16.h>
+
 #include "device_common.h"
 #include "packinfer.h"
 #include "sm100.cuh"
@@ -43,7 +45,13 @@
 #define PI_P_F16 0   // experiment: P packed as fp16 against bf16 V (idesc a_fmt = f16, b_fmt = bf16)
 #endif
 #ifndef PI_P_ROUNDED_SUM
-#define PI_P_ROUNDED_SUM 0   // 1: O normalised by the row sum of the bf16-rounded P (A/B: 7 % slower, profiles/r02a)
+#define PI_P_ROUNDED_SUM 2   // O normalised by the row sum of the bf16-rounded P: 1 = FHADD.BF16, 2 = PRMT + FADD2; 0 = exact sum
+#endif
+#ifndef PI_MERGE_ATOM
+#define PI_MERGE_ATOM 0   // merge counters: 0 atom.release, 1 atom.acq_rel, 2 one fence per unit + relaxed, 3 relaxed (A/B)
+#endif
+#ifndef PI_MERGE_WARP
+#define PI_MERGE_WARP 1   // A/B: 0 = no merge warp code, 2 = merge warp handshake only (timing, wrong results)
 #endif
 #ifndef PI_POLY_SAT
 #define PI_POLY_SAT 1
@@ -55,6 +63,8 @@
 namespace pi {
 
 using namespace sm100;
+
+constexpr float NEG_INF_F = -INFINITY;
 
 struct AttnParams {
   const pi_work* work_p;   // prefill work items (units [0, total_p))
@@ -120,9 +130,8 @@ struct AttnCfg {
   static constexpr int OFF_K = 2 * TILE_BYTES;
   static constexpr int OFF_V = OFF_K + NS * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
-  static constexpr int OFF_XCH = OFF_BAR + 256;       // single units: (m, l, l_rounded) of both warpgroups
-  static constexpr int OFF_FLAG = OFF_XCH + 2 * 128 * 16;   // single units: merge entry to finish per row
-  static constexpr int SMEM = OFF_FLAG + 128 * 4 + 1024;    // + alignment slack
+  static constexpr int OFF_XCH = OFF_BAR + 512;       // single units: (m, l, l_rounded) of both warpgroups
+  static constexpr int SMEM = OFF_XCH + 2 * 128 * 16 + 1024;  // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
   // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
   static constexpr uint32_t P1_SINGLE = F32 ? 64u : 96u;
@@ -154,7 +163,7 @@ struct AttnCfg {
 enum BarId {
   B_QFULL = 0, B_QFREE, B_KFULL0, B_KFULL1, B_KFREE0, B_KFREE1, B_VFULL0, B_VFULL1, B_VFREE0, B_VFREE1,
   B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
-  B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_COUNT
+  B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_EFULL0, B_EFREE0 = B_EFULL0 + 4, B_COUNT = B_EFREE0 + 4
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
@@ -187,6 +196,10 @@ __device__ __forceinline__ int snake_unit(int k, int b, int G) { return k * G + 
 
 // Unit w: prefill units first (each list is sorted by cost, descending), then decode units, so
 // the cheap decode units fill the tail of the one persistent launch (NEXT-3).
+// UK (unit kinds a kernel instance handles): 1 = pair units only (prefill launch, even r),
+// 2 = single-tile units only (decode launch, fp32 operands), 3 = both.  With one kind the
+// compiler drops the other kind's code from every role loop.
+template <int UK>
 __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
   Unit u;
   if (w >= p.total_p) {
@@ -206,10 +219,12 @@ __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
     u.head0 = u.kvh * p.r + tpu * hp;
     u.has_b = tpu == 2 && 2 * hp + 1 < p.r;
   }
+  if (UK == 1) u.has_b = true;
+  if (UK == 2) u.has_b = false;
   return u;
 }
 
-template <int D, bool F32>
+template <int D, bool F32, int UK>
 __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     packed_attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ) {
@@ -239,6 +254,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       mbar_init(&bar[B_OFULL0 + s], 1);
       mbar_init(&bar[B_OFREE0 + s], 128);
     }
+    for (int s = 0; s < 4; ++s) {   // merge hand-off ring (4 deep)
+      mbar_init(&bar[B_EFULL0 + s], 256);   // all softmax threads stored a single unit's partials
+      mbar_init(&bar[B_EFREE0 + s], 1);     // the merge warp took them
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -261,7 +280,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // The whole warp walks the schedule (uniform values); one elected lane issues each copy.
     uint32_t t = 0;
     for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-      const Unit u = get_unit(p, w);
+      const Unit u = get_unit<UK>(p, w);
       for (int s = 0; s < u.wk.span_count; ++s) {
         const pi_span sp = p.spans[u.wk.span_begin + s];
         for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
@@ -361,7 +380,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         __syncwarp();
       };
       for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-        const Unit u = get_unit(p, w);
+        const Unit u = get_unit<UK>(p, w);
         const int n = u.wk.n_ktiles;
         trace_unit(p, item, 0);
         mbar_wait(&bar[B_QFULL], item & 1);
@@ -473,7 +492,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // (one gather4 per 128-byte atom column) straight into the SWIZZLE_128B K-major operand layout.
     uint32_t item = 0;
     for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-      const Unit u = get_unit(p, w);
+      const Unit u = get_unit<UK>(p, w);
       const int nt = u.has_b ? 2 : 1;
       trace_unit(p, item, 4);
       mbar_wait(&bar[B_QFREE], (item & 1) ^ 1);
@@ -501,12 +520,116 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       ++item;
     }
   } else if (warp < C::ROLE) {
-    // ------------------------------------------------------------------ fp32 only: V^T staging
+    // ------------------------------------------------------------------ warp 3
     reg_dealloc<C::REG_ROLE>();
+    if (!F32 && (UK & 2) && PI_MERGE_WARP && p.merge_ctr != nullptr) {
+      // bf16: in-kernel LSE merge of split rows (packinfer_attention_merge; reading R10), off the
+      // softmax warps' path.  Per single-tile unit, after the softmax threads have stored its
+      // partials (EFULL ring), each lane takes rows of the unit with a partial slot and adds one
+      // to the (merge row, head) counter with acq_rel at GPU scope: CTA-scope acquire of the
+      // stores + the release of the atomic make them visible with it (cumulativity, as in a
+      // barrier-then-release split-K semaphore).  The lane completing the count owns the merge:
+      // the whole warp then merges it with lanes over channels - packinfer_merge's arithmetic in
+      // the same order, so outputs are bitwise equal to the separate merge - and re-zeroes the
+      // counter for the next launch.
+      uint32_t epi = 0;
+      for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+        const Unit u = get_unit<UK>(p, w);
+        if (u.has_b) continue;
+        const uint32_t e = epi & 3;
+        mbar_wait(&bar[B_EFULL0 + e], (epi >> 2) & 1);
+        if (PI_MERGE_ATOM == 2) __threadfence();
+        for (int r0 = 0; r0 < u.wk.row_count; r0 += 32) {
+          const int rr = r0 + lane;
+          int mm = -1, head = 0, qtok = 0;
+          if (rr < u.wk.row_count) {
+            const pi_row row = p.rows[u.wk.row_begin + rr];
+            const int slot = (row.out >> 4) - 1;
+            if (slot >= 0 && (PI_MERGE_WARP == 1 || PI_MERGE_WARP == 3)) {
+              const int m = p.slot_merge[slot];
+              head = u.head0 + (row.out & 15);
+              qtok = row.q_token;
+              uint32_t* ctr = p.merge_ctr + (int64_t)m * p.hq_count + head;
+              uint32_t old;
+              if (PI_MERGE_ATOM == 0)
+                asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+              else if (PI_MERGE_ATOM == 1)
+                asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+              else
+                asm volatile("atom.add.relaxed.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+              if (old + 1u == (uint32_t)p.merges[m].slot_count) {
+                *ctr = 0u;
+                mm = PI_MERGE_WARP == 3 ? -1 : m;   // 3: A/B, counters only
+              }
+            }
+          }
+          uint32_t todo = __ballot_sync(0xffffffffu, mm >= 0);
+          while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int m = __shfl_sync(0xffffffffu, mm, src);
+            const int h = __shfl_sync(0xffffffffu, head, src);
+            const pi_merge mg = p.merges[m];
+            float M = NEG_INF_F;
+            for (int bb = lane; bb < mg.slot_count; bb += 32)
+              M = fmaxf(M, __ldcg(&p.partial_lse[(int64_t)(mg.slot_begin + bb) * p.hq_count + h]));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            constexpr int V = D / 32;
+            float acc[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] = 0.f;
+            float W = 0.f;
+            if (M != NEG_INF_F) {
+              // slots in batches of MB: every load of a batch is in flight at once (a long split
+              // row has up to 32 slots), then the batch is accumulated in slot order
+              constexpr int MB = 4;
+              for (int b0 = 0; b0 < mg.slot_count; b0 += MB) {
+                float lw[MB], x[MB][V];
+#pragma unroll
+                for (int q = 0; q < MB; ++q) {
+                  if (b0 + q < mg.slot_count) {
+                    const int64_t sl = mg.slot_begin + b0 + q;
+                    lw[q] = __ldcg(&p.partial_lse[sl * p.hq_count + h]);
+                    const float* srcp = p.partial_o + (sl * p.hq_count + h) * D;
+#pragma unroll
+                    for (int i = 0; i < V; ++i) x[q][i] = __ldcg(srcp + lane + 32 * i);
+                  }
+                }
+#pragma unroll
+                for (int q = 0; q < MB; ++q) {
+                  if (b0 + q < mg.slot_count) {
+                    const float wgt = expf(lw[q] - M);
+                    W += wgt;
+#pragma unroll
+                    for (int i = 0; i < V; ++i) acc[i] += wgt * x[q][i];
+                  }
+                }
+              }
+            }
+            const float inv = W > 0.f ? 1.f / W : 0.f;
+            const int64_t o_el = (int64_t)mg.q_token * p.out_row_stride + (int64_t)h * D;
+            if (p.out_f32) {
+#pragma unroll
+              for (int i = 0; i < V; ++i) reinterpret_cast<float*>(p.out)[o_el + lane + 32 * i] = acc[i] * inv;
+            } else {
+#pragma unroll
+              for (int i = 0; i < V; ++i)
+                reinterpret_cast<__nv_bfloat16*>(p.out)[o_el + lane + 32 * i] = __float2bfloat16_rn(acc[i] * inv);
+            }
+            if (p.lse && lane == 0) p.lse[(int64_t)h * p.total_q + mg.q_token] = W > 0.f ? M + logf(W) : NEG_INF_F;
+            (void)qtok;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[B_EFREE0 + e]);
+        ++epi;
+      }
+    }
     if constexpr (F32) {
       uint32_t t = 0;
       for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-        const Unit u = get_unit(p, w);
+        const Unit u = get_unit<UK>(p, w);
         const float* vsrc = reinterpret_cast<const float*>(p.v_buf) + (int64_t)u.kvh * p.buffer_tokens * D;
         for (int s = 0; s < u.wk.span_count; ++s) {
           const pi_span sp = p.spans[u.wk.span_begin + s];
@@ -547,6 +670,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // two halves; pair units' one N = 128 chain completes SF[X][0] alone
     uint32_t cnt1[2] = {0, 0};
     uint32_t pvh = 0;                       // completions so far of PVH[X] (this slot's P.V halves)
+    uint32_t epi = 0;                       // units handed to the merge warp so far
     const float NEG_INF = -INFINITY;
     const float sl2 = p.scale_log2;
     // O_X *= alpha, all columns (lazy rescale; rare)
@@ -563,7 +687,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       }
     };
     for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-      const Unit u = get_unit(p, w);
+      const Unit u = get_unit<UK>(p, w);
       const pi_work& wk = u.wk;
       const int n = wk.n_ktiles;
       // pair units: warpgroup X owns tile X (both key halves); single-tile units: warpgroup X owns
@@ -649,7 +773,19 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               if (i & 1) acc1 = f2_add(acc1, e); else acc0 = f2_add(acc0, e);
               if constexpr (!F32) {
                 r[i] = pack_bf16(f2_lo(e), f2_hi(e));     // in place: i <= 2i
-                if (PI_P_ROUNDED_SUM) add_bf16x2(racc[2 * (i & 1)], racc[2 * (i & 1) + 1], r[i]);
+                if (PI_P_ROUNDED_SUM == 1) {
+                  add_bf16x2(racc[2 * (i & 1)], racc[2 * (i & 1) + 1], r[i]);
+                } else if (PI_P_ROUNDED_SUM == 2) {
+                  // the two rounded values as fp32 (bf16 = the high half of an fp32) by byte
+                  // permutes on the integer pipe, summed by one FADD2
+                  uint32_t lo, hi;
+                  asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(lo) : "r"(r[i]));
+                  asm("prmt.b32 %0, %1, 0, 0x3244;" : "=r"(hi) : "r"(r[i]));
+                  const uint64_t sum = f2_add(f2(racc[2 * (i & 1)], racc[2 * (i & 1) + 1]),
+                                              f2(__uint_as_float(lo), __uint_as_float(hi)));
+                  racc[2 * (i & 1)] = f2_lo(sum);
+                  racc[2 * (i & 1) + 1] = f2_hi(sum);
+                }
               } else {
                 r[2 * i] = __float_as_uint(f2_lo(e));
                 r[2 * i + 1] = __float_as_uint(f2_hi(e));
@@ -881,79 +1017,16 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
         }
       }
-      // in-kernel LSE merge (last arriver): this row's partial (both column halves + lse) is made
-      // visible device-wide before ONE atomic per (split row, head); the CTA completing the count
-      // merges every slot of the row with packinfer_merge's arithmetic and order (reading R10) and
-      // re-zeroes the counter for the next launch
-      const bool fused_merge = !u.has_b && p.merge_ctr != nullptr;
-      const bool part = valid && slot >= 0;
-      if (fused_merge && part) __threadfence();
       tc_fence_before();
       if (!u.has_b) named_bar_sync(1, 256);   // both warpgroups are done with O_0, O_1 and xch
       mbar_arrive(&bar[B_OFREE0 + X]);
-      if (fused_merge) {
-        int* flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
-        if (X == 0) {
-          int mm = -1;
-          if (part) {
-            const int m = p.slot_merge[slot];
-            uint32_t* ctr = p.merge_ctr + (int64_t)m * p.hq_count + head;
-            const uint32_t old = atomicAdd(ctr, 1u);
-            if (old + 1u == (uint32_t)p.merges[m].slot_count) {
-              *ctr = 0u;
-              __threadfence();
-              mm = m;
-            }
-          }
-          flag[row_id] = mm;
-        }
-        named_bar_sync(1, 256);
-        const int mm = flag[row_id];
-        if (part && mm >= 0) {
-          const pi_merge mg = p.merges[mm];
-          float M = NEG_INF;
-          for (int bb = 0; bb < mg.slot_count; ++bb)
-            M = fmaxf(M, __ldcg(&p.partial_lse[(int64_t)(mg.slot_begin + bb) * p.hq_count + head]));
-          constexpr int HD = D / 2;   // warpgroup X merges columns [X HD, (X + 1) HD)
-          float acc[HD];
-#pragma unroll
-          for (int i = 0; i < HD; ++i) acc[i] = 0.f;
-          float W = 0.f;
-          if (M != NEG_INF) {
-            for (int bb = 0; bb < mg.slot_count; ++bb) {
-              const int64_t sl = mg.slot_begin + bb;
-              const float w = expf(__ldcg(&p.partial_lse[sl * p.hq_count + head]) - M);
-              W += w;
-              const float4* src = reinterpret_cast<const float4*>(p.partial_o + (sl * p.hq_count + head) * D + X * HD);
-#pragma unroll
-              for (int v = 0; v < HD / 4; ++v) {
-                const float4 x = __ldcg(src + v);
-                acc[4 * v] += w * x.x;
-                acc[4 * v + 1] += w * x.y;
-                acc[4 * v + 2] += w * x.z;
-                acc[4 * v + 3] += w * x.w;
-              }
-            }
-          }
-          const float inv = W > 0.f ? 1.f / W : 0.f;
-          if (F32 || p.out_f32) {
-            float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)mg.q_token * p.out_row_stride + (int64_t)head * D +
-                                                             X * HD) * 4);
-#pragma unroll
-            for (int v = 0; v < HD / 4; ++v)
-              dst[v] = make_float4(acc[4 * v] * inv, acc[4 * v + 1] * inv, acc[4 * v + 2] * inv, acc[4 * v + 3] * inv);
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(p.out + ((int64_t)mg.q_token * p.out_row_stride + (int64_t)head * D +
-                                                           X * HD) * 2);
-#pragma unroll
-            for (int v = 0; v < HD / 8; ++v)
-              dst[v] = make_uint4(pack_bf16(acc[8 * v] * inv, acc[8 * v + 1] * inv),
-                                  pack_bf16(acc[8 * v + 2] * inv, acc[8 * v + 3] * inv),
-                                  pack_bf16(acc[8 * v + 4] * inv, acc[8 * v + 5] * inv),
-                                  pack_bf16(acc[8 * v + 6] * inv, acc[8 * v + 7] * inv));
-          }
-          if (X == 0 && p.lse) p.lse[(int64_t)head * p.total_q + mg.q_token] = W > 0.f ? M + logf(W) : NEG_INF;
-        }
+      if ((UK & 2) && PI_MERGE_WARP && !u.has_b && p.merge_ctr != nullptr) {
+        // in-kernel merge: hand this unit's partials (both column halves + lse, stored above) to the
+        // merge warp (ring of 4; the mbarrier arrive releases the stores at CTA scope)
+        const uint32_t e = epi & 3;
+        mbar_wait(&bar[B_EFREE0 + e], ((epi >> 2) & 1) ^ 1);
+        mbar_arrive(&bar[B_EFULL0 + e]);
+        ++epi;
       }
       if (u.has_b) {
         cnt[0] += n;
@@ -978,6 +1051,22 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
 }
 
 unsigned long long* g_debug_trace = nullptr;
+
+template <int D, bool F32, int UK>
+static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                               const CUtensorMap& tmQ, int grid, cudaStream_t stream) {
+  using C = AttnCfg<D, F32>;
+  if constexpr (F32 && UK != 2) {
+    return fail(PI_EUNSUP, "fp32 operands run single-tile units only");
+  } else {
+    static std::atomic<int> smem_opt_in[kMaxDevices];   // per template instance and device
+    pi_status s = set_max_dynamic_smem(reinterpret_cast<const void*>(packed_attention_kernel<D, F32, UK>),
+                                       smem_opt_in, C::SMEM);
+    if (s != PI_OK) return s;
+    packed_attention_kernel<D, F32, UK><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ);
+    return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
+  }
+}
 
 // mode: bit 0 = prefill work items, bit 1 = decode work items (both = one fused launch)
 template <int D, bool F32>
@@ -1016,7 +1105,8 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   p.trace = g_debug_trace;
   p.merges = dp->merges;
   p.slot_merge = dp->slot_merge;
-  p.merge_ctr = (dp->n_merges > 0 && (mode & 2)) ? merge_ctr : nullptr;
+  // fp32 operands: warp 3 stages V^T, so the entry point merges with a separate launch instead
+  p.merge_ctr = (!F32 && dp->n_merges > 0 && (mode & 2)) ? merge_ctr : nullptr;
 
   CUtensorMap tmK, tmV;
   const CUtensorMapDataType dt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -1036,13 +1126,15 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   s = encode_tmap_2d(&tmQ, dt, q, qdims, qstrides, qbox, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
 
-  static std::atomic<int> smem_opt_in[kMaxDevices];   // per template instance and device
-  s = set_max_dynamic_smem(reinterpret_cast<const void*>(packed_attention_kernel<D, F32>), smem_opt_in, C::SMEM);
-  if (s != PI_OK) return s;
   const int64_t total = (int64_t)p.total_p + (int64_t)p.n_work_d * p.units_d;
   const int grid = (int)std::min<int64_t>(total, num_sms());
-  packed_attention_kernel<D, F32><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ);
-  return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
+  // kernel instance by the unit kinds present (see get_unit): a prefill-only launch with even r
+  // has pair units only, a decode-only launch (or fp32 operands) single-tile units only
+  const bool pairs_only = !F32 && p.n_work_d == 0 && (r % 2) == 0;
+  const bool singles_only = F32 || p.n_work_p == 0 || r == 1;
+  if (pairs_only) return launch_kernel<D, F32, 1>(p, tmK, tmV, tmQ, grid, stream);
+  if (singles_only) return launch_kernel<D, F32, 2>(p, tmK, tmV, tmQ, grid, stream);
+  return launch_kernel<D, F32, 3>(p, tmK, tmV, tmQ, grid, stream);
 }
 
 static pi_status attention_entry(int mode, const pi_device_plan* dp, const void* q, int64_t q_row_stride,
@@ -1130,8 +1222,14 @@ pi_status packinfer_attention_merge(const pi_device_plan* dp, const void* q, int
                                     float softmax_scale, pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
                                     float* partial_o, float* partial_lse, uint32_t* merge_counters,
                                     pi_stream_t stream) {
-  return pi::attention_entry(3, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim, softmax_scale,
-                             dt, out, out_row_stride, lse, partial_o, partial_lse, stream, merge_counters, true);
+  pi_status s = pi::attention_entry(3, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim,
+                                    softmax_scale, dt, out, out_row_stride, lse, partial_o, partial_lse, stream,
+                                    merge_counters, true);
+  // fp32 operands (the toy config): warp 3 stages V^T there, so the merge is a separate launch
+  if (s == PI_OK && dt == PI_FP32 && dp->n_merges > 0)
+    s = packinfer_merge(dp, partial_o, partial_lse, hkv_count * gqa_ratio, head_dim, dt, out, out_row_stride, lse,
+                        stream);
+  return s;
 }
 
 }  // extern "C"

@@ -391,8 +391,13 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   std::vector<int32_t> item_seg;   // first row segment of each decode item: one segment per member
   std::vector<int32_t> dm;         // scratch: decode members of a prefix entry
   auto emit_decode = [&](int32_t g, const int32_t* reqs, int32_t n_reqs, int64_t b, int64_t len) {
-    for (int64_t c0 = 0; c0 < len; c0 += chunk) {
-      const int64_t cl = std::min<int64_t>(chunk, len - c0);
+    // ceil(len / chunk) chunks of near-equal tile counts (not full chunks + a short remainder):
+    // the chunks of one span then sit next to each other in the LPT order, so a split row's last
+    // partial lands with the others instead of in the launch's tail
+    const int64_t n_tiles = ceil_div(len, TK), n_chunks = std::max<int64_t>(1, ceil_div(len, chunk));
+    for (int64_t q = 0, c0 = 0; q < n_chunks && c0 < len; ++q) {
+      const int64_t tiles_q = n_tiles / n_chunks + (q < n_tiles % n_chunks ? 1 : 0);
+      const int64_t cl = std::min<int64_t>(tiles_q * TK, len - c0);
       pi_work w{};
       w.kind = 1;
       w.group = g;
@@ -411,6 +416,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       w.span_count = 1;
       w.n_ktiles = (int32_t)ceil_div(cl, TK);
       dwork.push_back(w);
+      c0 += cl;
     }
   };
   const int32_t per_block = std::max(1, TQ / r);

@@ -443,13 +443,14 @@ class PackedBatch:
             relayout: bool = True, fused: bool = True, kernel_merge: Optional[bool] = None):
         """relayout -> attention -> merge.  fused: ONE attention launch over prefill and decode work
         items (packinfer_attention); else one launch per kind (prefill, then decode).  kernel_merge
-        (default: = fused): the LSE merge of split rows inside that launch
-        (packinfer_attention_merge) instead of a packinfer_merge launch."""
+        (default False): the LSE merge of split rows inside that launch (packinfer_attention_merge)
+        instead of a packinfer_merge launch (bitwise equal; the separate launch is faster on long
+        split rows, profiles/r02b)."""
         if relayout:
             packinfer_relayout_kv(self.dp, k_paged, v_paged, block_table, self.k_buf, self.v_buf,
                                   hkv_begin, self.hkv, stream)
         if kernel_merge is None:
-            kernel_merge = fused
+            kernel_merge = False
         if fused and kernel_merge:
             packinfer_attention_merge(self.dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o,
                                       self.partial_lse, self.merge_counters, self.r, 0.0, stream)

@@ -1,4 +1,5 @@
-"""CTA-0 timeline of the packed attention kernel on the cfg3 decode batch (debug hook)."""
+"""CTA-0 timeline of the packed attention kernel on a decode batch (debug hook).
+    python scripts/trace_decode.py [cfg3|cfg4_decode]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 # the trace hooks are compiled in only with -DPI_TRACE=1: build that variant and load it
@@ -13,9 +14,11 @@ import numpy as np, torch
 from synth import workloads as W
 from paper_2602_06072_b200 import packinfer as pk
 
-b = W.cfg3_decode(1)
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+b = W.make_batch(name)
 t = W.make_tensors(b, device="cuda")
-pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq // b.hkv, b.d, torch.bfloat16, "cuda")
+pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq // b.hkv, b.d, torch.bfloat16, "cuda",
+                    headroom=32 if "cfg4" in name else 0)
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 tr = torch.zeros(64 * 24 + 64 * 8, dtype=torch.int64, device="cuda")
@@ -33,9 +36,10 @@ w = pb.plan.decode_work
 print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done   (n_ktiles rows)")
 for i in range(30):
     r = U[i]
-    item = (i * 148) // 8
+    # snake order: CTA 0 takes unit k*148 (even k) / k*148+147 (odd k)
+    item = ((i * 148) if i % 2 == 0 else (i * 148 + 147)) // b.hkv
     print(f"{i:4d} " + " ".join(f"{(v - u0 if v else -1):9d}" for v in r[:7]),
           int(w[item]["n_ktiles"]) if item < len(w) else -1, int(w[item]["row_count"]) if item < len(w) else -1)
 t0 = a[a > 0].min() if (a > 0).any() else 0
-print("softmax A per tile (gotS -> arriveP):", [int(x) for x in (a[:30, 9] - a[:30, 7])])
+print("softmax A per tile (gotS -> arriveP half 1):", [int(x) for x in (a[:30, 9] - a[:30, 7])])
 print("softmax A wait S:", [int(x) for x in (a[:30, 7] - a[:30, 6])])
