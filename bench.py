@@ -178,8 +178,11 @@ class Runner:
         self.hkv_begin, self.hkv_count = hkv_begin, hkv_count
         self.t = W.make_tensors(b, device=device, seed=seed)
         dt = self.t["q"].dtype
+        flags = int(os.environ.get("PI_BENCH_PLAN_FLAGS", "0"))      # A/B hook (ablations)
+        chunk = int(os.environ.get("PI_BENCH_DECODE_CHUNK", "1024"))  # A/B hook
         self.pbs = [pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, hkv_count, self.r, b.d, dt,
-                                   device, capacity=capacity, headroom=headroom) for _ in range(2)]
+                                   device, capacity=capacity, headroom=headroom, flags=flags, decode_chunk=chunk)
+                    for _ in range(2)]
         self.events = [torch.cuda.Event() for _ in range(2)]
         for e in self.events:
             e.record()

@@ -102,6 +102,9 @@ typedef struct {
  * "unpacked compute" baseline.  Groups, layout and results are unchanged; only tile count and
  * tile efficiency change.                                                                     */
 #define PI_PLAN_NO_QPACK 1
+/* Option: pack consecutive short decode suffixes of one group into one decode work item (key span =
+ * their hull <= decode_chunk, per-row [lo, hi) = own suffix).  Off by default (measured slower).   */
+#define PI_PLAN_DPACK 2
 
 /* Fill *cfg with the defaults: C=8192, G auto, no M_max, delta=0, 128/128 tiles,
  * decode_chunk=1024, gqa_ratio=1. */

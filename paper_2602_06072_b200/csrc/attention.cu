@@ -109,9 +109,11 @@ __device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int
   if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
     p.trace[tile * 24 + ev] = clock64();
 }
-// Per-unit events: trace[1024 + unit * 8 + ev], first 64 units of CTA 0.
+// Per-unit events: trace[1536 + unit * 16 + ev], first 64 units of CTA 0 (0-3 MMA issuer, 4-6 Q
+// gather, 7-11 softmax warp 4: unit start, first S landed, epilogue start (O landed), O read,
+// epilogue done).
 __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
-  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[64 * 24 + unit * 8 + ev] = clock64();
+  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[64 * 24 + unit * 16 + ev] = clock64();
 }
 
 template <int D, bool F32>
@@ -279,10 +281,25 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     reg_dealloc<C::REG_ROLE>();
     // The whole warp walks the schedule (uniform values); one elected lane issues each copy.
     uint32_t t = 0;
+    // next unit's work item + first span loaded one unit ahead (as in the softmax warps)
+    Unit nu;
+    pi_span nsp = {0, 0};
+    if ((int)blockIdx.x < total) {
+      nu = get_unit<UK>(p, blockIdx.x);
+      nsp = p.spans[nu.wk.span_begin];
+    }
     for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-      const Unit u = get_unit<UK>(p, w);
+      const Unit u = nu;
+      const pi_span span0 = nsp;
+      {
+        const int wn = snake_unit(k + 1, blockIdx.x, gridDim.x);
+        if (wn < total) {
+          nu = get_unit<UK>(p, wn);
+          nsp = p.spans[nu.wk.span_begin];
+        }
+      }
       for (int s = 0; s < u.wk.span_count; ++s) {
-        const pi_span sp = p.spans[u.wk.span_begin + s];
+        const pi_span sp = s == 0 ? span0 : p.spans[u.wk.span_begin + s];
         for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
           const int st = t % C::NS;
           const uint32_t ph = (t / C::NS) & 1;
@@ -379,8 +396,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         }
         __syncwarp();
       };
+      Unit nu;
+      if ((int)blockIdx.x < total) nu = get_unit<UK>(p, blockIdx.x);
       for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-        const Unit u = get_unit<UK>(p, w);
+        const Unit u = nu;   // loaded one unit ahead
+        {
+          const int wn = snake_unit(k + 1, blockIdx.x, gridDim.x);
+          if (wn < total) nu = get_unit<UK>(p, wn);
+        }
         const int n = u.wk.n_ktiles;
         trace_unit(p, item, 0);
         mbar_wait(&bar[B_QFULL], item & 1);
@@ -686,8 +709,26 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         tmem_st32(o_tm + c4 * 32, o32);
       }
     };
+    // The next unit's descriptor (work item, this thread's row, first key span) is loaded one unit
+    // ahead: its global-load latency (~2 dependent L2 round trips) hides behind the current unit
+    // instead of opening every unit (a 1-tile decode unit is otherwise mostly that latency).
+    Unit nu;
+    pi_row nrow = {0, 0, 0, 0};
+    pi_span nsp = {0, 0};
+    auto prefetch = [&](int wn) {
+      nu = get_unit<UK>(p, wn);
+      nrow = row_id < nu.wk.row_count ? p.rows[nu.wk.row_begin + row_id] : pi_row{0, 0, 0, 0};
+      nsp = p.spans[nu.wk.span_begin];
+    };
+    if ((int)blockIdx.x < total) prefetch(blockIdx.x);
     for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
-      const Unit u = get_unit<UK>(p, w);
+      const Unit u = nu;
+      const pi_row row_pf = nrow;
+      const pi_span span0 = nsp;
+      {
+        const int wn = snake_unit(k + 1, blockIdx.x, gridDim.x);
+        if (wn < total) prefetch(wn);
+      }
       const pi_work& wk = u.wk;
       const int n = wk.n_ktiles;
       // pair units: warpgroup X owns tile X (both key halves); single-tile units: warpgroup X owns
@@ -695,12 +736,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       const int h_lo = u.has_b ? 0 : X, h_hi = u.has_b ? 2 : X + 1;
       const bool valid = row_id < wk.row_count;
       const bool warp_any = wq * 32 < wk.row_count;
-      pi_row row = {0, 0, 0, 0};
-      if (valid) row = p.rows[wk.row_begin + row_id];
+      const pi_row row = row_pf;
       float m_ref = NEG_INF, l = 0.f, lr = 0.f;   // running max (log2 units), exact / rounded-P sums
       uint32_t j = 0;
+      if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 7);
       for (int s = 0; s < wk.span_count; ++s) {
-        const pi_span sp = p.spans[wk.span_begin + s];
+        const pi_span sp = s == 0 ? span0 : p.spans[wk.span_begin + s];
         const bool last = (s == wk.span_count - 1);
         const int se = sp.begin + sp.len;
         for (int k0 = sp.begin; k0 < se; k0 += 128, ++j) {
@@ -739,6 +780,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt1[b] + kb) & 1);
           tc_fence_after();
           if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
+          if (j == 0 && warp == C::ROLE && lane == 0) trace_unit(p, ix, 8);
           if (warp_any) {
             load_s(region + 64u * h_lo);
             tmem_wait_ld();
@@ -929,6 +971,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       // ---------------- epilogue: O / l -> out (or partial), lse
       mbar_wait(&bar[B_OFULL0 + X], ix & 1);
       tc_fence_after();
+      if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 9);
       const int slot = (row.out >> 4) - 1;
       const int head = u.head0 + (u.has_b ? X : 0) + (row.out & 15);
       // pair units: out = O_X / l.  Single units: the two warpgroups hold (m, l) of key halves
@@ -1017,9 +1060,11 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
         }
       }
+      if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 10);
       tc_fence_before();
       if (!u.has_b) named_bar_sync(1, 256);   // both warpgroups are done with O_0, O_1 and xch
       mbar_arrive(&bar[B_OFREE0 + X]);
+      if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 11);
       if ((UK & 2) && PI_MERGE_WARP && !u.has_b && p.merge_ctr != nullptr) {
         // in-kernel merge: hand this unit's partials (both column halves + lse, stored above) to the
         // merge warp (ring of 4; the mbarrier arrive releases the stores at CTA scope)

@@ -67,6 +67,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const int32_t TQ = cfg->tile_q, TK = cfg->tile_k;
   const int64_t chunk = cfg->decode_chunk;
   const bool no_qpack = (cfg->flags & PI_PLAN_NO_QPACK) != 0;
+  const bool dpack = (cfg->flags & PI_PLAN_DPACK) != 0;
   if (C < 1) return fail(PI_EINVAL, "capacity must be >= 1");
   if (delta < 0 || cfg->num_groups < 0 || cfg->mem_cap < 0)
     return fail(PI_EINVAL, "negative headroom / num_groups / mem_cap");
@@ -75,7 +76,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   if (TQ != 128 || TK != 128) return fail(PI_EINVAL, "tile_q and tile_k must be 128");
   if (chunk < TK || chunk % TK) return fail(PI_EINVAL, "decode_chunk must be a positive multiple of tile_k");
   if (r < 1 || r > 16) return fail(PI_EINVAL, "gqa_ratio must be in [1, 16]");
-  if (cfg->flags & ~PI_PLAN_NO_QPACK) return fail(PI_EINVAL, "unknown pi_config.flags bits");
+  if (cfg->flags & ~(PI_PLAN_NO_QPACK | PI_PLAN_DPACK)) return fail(PI_EINVAL, "unknown pi_config.flags bits");
   int64_t total_q = 0;
   for (int32_t i = 0; i < n; ++i) {
     const int32_t L = kv_len[i], q = q_len[i];
@@ -428,11 +429,44 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
     spans.reserve(spans.size() + est);
     segs.reserve(segs.size() + est + (size_t)n);
   }
+  // PI_PLAN_DPACK (opt-in): packed decode items (the decode analogue of packed prefill tiles,
+  // P:150): consecutive decode suffixes of one group - adjacent in B_g up to the headroom between
+  // them - share ONE item whose key span is their hull (<= decode_chunk keys, <= tile_q rows);
+  // each row sees only its own suffix [lo, hi).  Every key is still read once.  Measured slower
+  // on configs[3] (fewer, longer units balance worse: profiles/r02d/ab_plan.txt), so off by default.
+  struct PackMember { int32_t req; int64_t b, len; };
+  std::vector<PackMember> pack;
+  auto flush_pack = [&](int32_t g) {
+    if (pack.empty()) return;
+    if (pack.size() == 1) {
+      emit_decode(g, &pack[0].req, 1, pack[0].b, pack[0].len);
+    } else {
+      const int64_t hb = pack.front().b, he = pack.back().b + pack.back().len;
+      pi_work w{};
+      w.kind = 1;
+      w.group = g;
+      w.row_begin = n_rows;
+      w.span_begin = (int32_t)spans.size();
+      add_span(hb, he - hb);
+      item_seg.push_back((int32_t)segs.size());
+      for (const PackMember& m : pack) {
+        segs.push_back({n_rows, r, (int32_t)q_off[m.req], (int32_t)m.b, (int32_t)(m.b + m.len), 0, PI_SEG_DECODE, m.req});
+        n_rows += r;
+        dcount[m.req] += 1;
+      }
+      w.row_count = n_rows - w.row_begin;
+      w.span_count = 1;
+      w.n_ktiles = (int32_t)ceil_div(he - hb, TK);
+      dwork.push_back(w);
+    }
+    pack.clear();
+  };
   for (int32_t g = 0; g < G; ++g) {
     const auto& ent = entries[g];
     for (size_t a = 0; a < ent.size(); ++a) {
       const Entry& e = ent[a];
       if (e.ctx >= 0 && e.first_of_ctx) {  // shared prefix: read once for all decode members
+        flush_pack(g);
         dm.clear();
         for (size_t b = a; b < ent.size() && ent[b].ctx == e.ctx; ++b)
           if (q_len[pieces[ent[b].piece].request] == 1) dm.push_back(pieces[ent[b].piece].request);
@@ -442,10 +476,21 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
                       offsets[e.piece].l_prefix);
       }
       const Piece& pc = pieces[e.piece];
-      if (q_len[pc.request] != 1) continue;
+      if (q_len[pc.request] != 1) {   // a prefill suffix sits between: not adjacent any more
+        flush_pack(g);
+        continue;
+      }
       const bool last_piece = e.piece == first_piece[pc.request + 1] - 1;
-      emit_decode(g, &pc.request, 1, piece_buf(e.piece), offsets[e.piece].l_suffix + (last_piece ? app(pc.request) : 0));
+      const int64_t b = piece_buf(e.piece), len = offsets[e.piece].l_suffix + (last_piece ? app(pc.request) : 0);
+      if (!dpack || len >= chunk) {   // one item per suffix (default), or a long suffix chunked on its own
+        flush_pack(g);
+        emit_decode(g, &pc.request, 1, b, len);
+        continue;
+      }
+      if (!pack.empty() && (b + len - pack.front().b > chunk || (int64_t)(pack.size() + 1) * r > TQ)) flush_pack(g);
+      pack.push_back({pc.request, b, len});
     }
+    flush_pack(g);
   }
   // partial slots for rows with more than one decode item (reading R10 / Q19)
   std::vector<int32_t> slot_base(n, -1), occ(n, 0);

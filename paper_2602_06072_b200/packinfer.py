@@ -48,6 +48,7 @@ class pi_config(C.Structure):
 
 
 PI_PLAN_NO_QPACK = 1   # ablation: one Q tile set per request (include/packinfer.h)
+PI_PLAN_DPACK = 2      # option: pack short decode suffixes of a group into one decode item
 
 
 PIECE_DT = np.dtype([("request", "<i4"), ("piece", "<i4"), ("kv_begin", "<i4"), ("kv_len", "<i4"), ("group", "<i4")])
@@ -375,10 +376,10 @@ class PackedBatch:
 
     def __init__(self, kv_len, q_len, prefix_id, prefix_len, hkv_count: int, gqa_ratio: int, head_dim: int,
                  dtype, device, capacity: int = 8192, headroom: int = 0, num_groups: int = 0,
-                 decode_chunk: int = 1024, mem_cap: int = 0):
+                 decode_chunk: int = 1024, mem_cap: int = 0, flags: int = 0):
         import torch
         self.cfg = default_config(capacity=capacity, headroom=headroom, num_groups=num_groups,
-                                  decode_chunk=decode_chunk, gqa_ratio=gqa_ratio, mem_cap=mem_cap)
+                                  decode_chunk=decode_chunk, gqa_ratio=gqa_ratio, mem_cap=mem_cap, flags=flags)
         self.args = (kv_len, q_len, prefix_id, prefix_len)
         self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, pinned=True)
         # Two pinned host arenas alternate: a plan is never rewritten while its asynchronous upload

@@ -21,7 +21,7 @@ pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq //
                     headroom=32 if "cfg4" in name else 0)
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
-tr = torch.zeros(64 * 24 + 64 * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(64 * 24 + 64 * 16, dtype=torch.int64, device="cuda")
 L = pk.lib()
 L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
 L.packinfer_debug_trace(tr.data_ptr())
@@ -30,15 +30,15 @@ torch.cuda.synchronize()
 L.packinfer_debug_trace(None)
 A = tr.cpu().numpy().astype(np.int64)
 a = A[:64 * 24].reshape(64, 24)
-U = A[64 * 24:].reshape(64, 8)
+U = A[64 * 24:].reshape(64, 16)
 u0 = U[U > 0].min()
 w = pb.plan.decode_work
-print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done   (n_ktiles rows)")
+print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done  sm_start sm_gotS0 sm_epi  sm_Oread sm_epidone (n_ktiles rows)")
 for i in range(30):
     r = U[i]
     # snake order: CTA 0 takes unit k*148 (even k) / k*148+147 (odd k)
     item = ((i * 148) if i % 2 == 0 else (i * 148 + 147)) // b.hkv
-    print(f"{i:4d} " + " ".join(f"{(v - u0 if v else -1):9d}" for v in r[:7]),
+    print(f"{i:4d} " + " ".join(f"{(v - u0 if v else -1):9d}" for v in r[:12]),
           int(w[item]["n_ktiles"]) if item < len(w) else -1, int(w[item]["row_count"]) if item < len(w) else -1)
 t0 = a[a > 0].min() if (a > 0).any() else 0
 print("softmax A per tile (gotS -> arriveP half 1):", [int(x) for x in (a[:30, 9] - a[:30, 7])])

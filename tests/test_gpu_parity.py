@@ -515,3 +515,25 @@ def test_in_kernel_merge_bitwise(seed):
             assert torch.equal(l0, l1)
     ro, rl = H.oracle_full(b, t)
     H.compare(*res["kernel", torch.float32], ro, rl)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_packed_decode_items_option(seed):
+    """PI_PLAN_DPACK: short decode suffixes of one group packed into one decode item (per-row
+    [lo, hi) inside the hull) - same results as the oracle, fewer decode items."""
+    from paper_2602_06072_b200 import packinfer as pk
+    b = W.random_batch(700 + seed, n=20, max_len=900, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    t = W.make_tensors(b, device="cuda")
+    r = b.hq // b.hkv
+    res = {}
+    for flags in (0, pk.PI_PLAN_DPACK):
+        pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16, "cuda",
+                            capacity=2048, decode_chunk=512, headroom=3, flags=flags)
+        out = torch.full((b.total_q, b.hq, b.d), float("nan"), dtype=torch.float32, device="cuda")
+        lse = torch.full((b.hq, b.total_q), float("nan"), dtype=torch.float32, device="cuda")
+        pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out, lse)
+        torch.cuda.synchronize()
+        res[flags] = (out, lse, int(pb.plan.c.n_decode_work))
+    assert res[pk.PI_PLAN_DPACK][2] < res[0][2]
+    ro, rl = H.oracle_full(b, t)
+    H.compare(res[pk.PI_PLAN_DPACK][0], res[pk.PI_PLAN_DPACK][1], ro, rl)
