@@ -756,6 +756,7 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
     if dist_on:
         rms, rk = max_over_ranks(dev, rms, rk)
     c = rd.pbs[0].plan.c
+    paged = paged_decode(bd, rd, dev, h0, hc, steps, args.warmup, dist_on)
     out = {"ms_per_step": dms, "kernel_ms": dec_ms, "kv_bytes": kvb, "qo_bytes": qob, "achieved_gbs": ach,
            "peak_gbs": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
            "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9, "work_items": int(c.n_decode_work),
@@ -766,9 +767,59 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
                         "step_gbs": (kvb + qob) / (rms * 1e-3) / 1e9,
                         "gpu_launches_per_step": rd.launches_per_step - 1,
                         "note": "KV resident in the group-contiguous layout: plan + upload (+ row expansion) "
-                                "+ one attention launch + merge; no relayout"}}
+                                "+ one attention launch + merge; no relayout"},
+           "paged": paged}
     del rd
     return out
+
+
+def paged_decode(bd, rd, dev, h0, hc, steps, warmup, dist_on):
+    """NEXT-4 ablation ("packed I/O" off, Fig. breakdown): the same decode batch planned
+    with PI_PLAN_PAGED and decoded straight from the paged cache (packinfer_attention_decode_paged:
+    no consolidation, no prefix co-location; the same tcgen05 kernel).  Step = plan + upload +
+    attention + merge; bytes = every request's logical KV (prefixes read once per request)."""
+    import torch
+    from paper_2602_06072_b200 import packinfer as pk
+    r = bd.hq // bd.hkv
+    pb = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, r, bd.d, torch.bfloat16, dev,
+                        flags=pk.PI_PLAN_PAGED)
+    pb.k_buf = pb.v_buf = None                       # no group buffers in this mode
+    st = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    kern = []
+
+    def once(timed):
+        pb.replan(st)
+        a, e = ev(), ev()
+        a.record(st)
+        pk.packinfer_attention_decode_paged(pb.dp, rd.q, rd.t["k_paged"], rd.t["v_paged"], rd.t["block_table"],
+                                            rd.out, rd.lse, pb.partial_o, pb.partial_lse, r, h0, hc, 0.0, st)
+        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, rd.out, rd.lse, st)
+        e.record(st)
+        if timed:
+            kern.append((a, e))
+
+    for _ in range(warmup):
+        once(False)
+    torch.cuda.synchronize()
+    s0, s1 = ev(), ev()
+    s0.record(st)
+    for _ in range(steps):
+        once(True)
+    s1.record(st)
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / steps
+    kms = sum(a.elapsed_time(e) for a, e in kern) / len(kern)
+    if dist_on:
+        ms, kms = max_over_ranks(dev, ms, kms)
+    kv_tokens = int(bd.kv_len.sum())
+    kvb = 2 * kv_tokens * hc * bd.d * 2
+    qob = 2 * bd.n * hc * r * bd.d * 2
+    del pb
+    return {"ms_per_step": ms, "kernel_ms": kms, "kv_tokens": kv_tokens, "kv_bytes": kvb,
+            "achieved_gbs": (kvb + qob) / (kms * 1e-3) / 1e9, "work_items": None,
+            "note": "PI_PLAN_PAGED: decode straight from the paged cache, no relayout, no prefix co-location "
+                    "(attention + merge kernel time; step = plan + upload + attention + merge)"}
 
 
 def section_prefill(name, dev, h0, hc, args, peaks, dist_on, sampler, seed_rank):

@@ -105,6 +105,11 @@ typedef struct {
 /* Option: pack consecutive short decode suffixes of one group into one decode work item (key span =
  * their hull <= decode_chunk, per-row [lo, hi) = own suffix).  Off by default (measured slower).   */
 #define PI_PLAN_DPACK 2
+/* Ablation (NEXT-4, Fig. "breakdown" P:480-489: "packed I/O" off): a decode-only plan whose work
+ * items cover each request's LOGICAL tokens, read straight from the paged cache by
+ * packinfer_attention_decode_paged - no consolidation and no prefix co-location.  Groups, offsets
+ * and the copy plan are still computed (unused).  q_len must be 1 for every request.           */
+#define PI_PLAN_PAGED 4
 
 /* Fill *cfg with the defaults: C=8192, G auto, no M_max, delta=0, 128/128 tiles,
  * decode_chunk=1024, gqa_ratio=1. */
@@ -295,6 +300,20 @@ PI_API pi_status packinfer_attention(const pi_device_plan* dp, const void* q, in
                                      int32_t gqa_ratio, int32_t head_dim, float softmax_scale,
                                      pi_dtype dt, void* out, int64_t out_row_stride, float* lse,
                                      float* partial_o, float* partial_lse, pi_stream_t stream);
+
+/* Packed decode straight from the paged KV cache (NEXT-4 ablation; plans made with PI_PLAN_PAGED):
+ * the same kernel as packinfer_attention_decode, but each 128-key tile is one TMA box of the
+ * paged cache k/v_paged [num_blocks, page_size, hkv_total, head_dim] at the block the request's
+ * block_table row maps (page_size a multiple of 128).  KV heads [hkv_begin, hkv_begin+hkv_count);
+ * q/out/partials as in packinfer_attention_decode.  PI_BF16 / PI_BF16_OUT_F32, head_dim 64/128. */
+PI_API pi_status packinfer_attention_decode_paged(const pi_device_plan* dp, const void* q, int64_t q_row_stride,
+                                                  const void* k_paged, const void* v_paged,
+                                                  const int32_t* block_table, int32_t max_blocks,
+                                                  int32_t page_size, int32_t num_blocks, int32_t hkv_total,
+                                                  int32_t hkv_begin, int32_t hkv_count, int32_t gqa_ratio,
+                                                  int32_t head_dim, float softmax_scale, pi_dtype dt, void* out,
+                                                  int64_t out_row_stride, float* lse, float* partial_o,
+                                                  float* partial_lse, pi_stream_t stream);
 
 /* Fully fused form (NEXT-3; "reducing ... kernel launch overhead"): as
  * packinfer_attention, and the LSE merge of split rows happens inside the same launch - the CTA

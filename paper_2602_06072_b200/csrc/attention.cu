@@ -96,7 +96,18 @@ struct AttnParams {
   const pi_merge* merges;
   const int32_t* slot_merge;
   uint32_t* merge_ctr;     // [n_merges * hq_count], zero on entry and on exit
+  // paged mode (packinfer_attention_decode_paged): K/V tiles straight from the paged cache
+  const int32_t* block_table;   // NULL = group-contiguous buffers
+  int32_t max_blocks, page, kv_head0;
 };
+
+// One paged-mode tile: logical keys [k0, k0 + 128) of block-table row `row` = 128 consecutive slots
+// of one page (k0 a multiple of 128, page a multiple of 128); returns the token coordinate of the
+// paged tensor map.
+__device__ __forceinline__ int paged_token(const AttnParams& p, int row, int k0) {
+  const int blk = __ldg(&p.block_table[(int64_t)row * p.max_blocks + k0 / p.page]);
+  return blk * p.page + k0 % p.page;
+}
 
 // Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
 constexpr int TRACE_TILES = 64;
@@ -303,13 +314,19 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
           const int st = t % C::NS;
           const uint32_t ph = (t / C::NS) & 1;
+          // coordinates: buffers (d, token, kv head); paged cache (d, kv head, page slot)
+          int c1 = k0, c2 = u.kvh;
+          if (p.block_table != nullptr) {
+            c1 = p.kv_head0 + u.kvh;
+            c2 = paged_token(p, u.wk.reserved, k0);
+          }
           mbar_wait(&bar[B_KFREE0 + st], ph ^ 1);
           if (elect_one()) {
             mbar_arrive_expect_tx(&bar[B_KFULL0 + st], C::TILE_BYTES);
 #pragma unroll
             for (int a = 0; a < C::ATOMS; ++a)
               tma_load_3d(smem + C::OFF_K + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmK, &bar[B_KFULL0 + st],
-                          a * C::ATOM_ELEMS, k0, u.kvh);
+                          a * C::ATOM_ELEMS, c1, c2);
           }
           __syncwarp();
           if constexpr (!F32) {
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
 #pragma unroll
               for (int a = 0; a < C::ATOMS; ++a)
                 tma_load_3d(smem + C::OFF_V + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmV, &bar[B_VFULL0 + st],
-                            a * C::ATOM_ELEMS, k0, u.kvh);
+                            a * C::ATOM_ELEMS, c1, c2);
             }
             __syncwarp();
           }
@@ -1114,11 +1131,16 @@ static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, cons
 }
 
 // mode: bit 0 = prefill work items, bit 1 = decode work items (both = one fused launch)
+struct PagedSrc {   // packinfer_attention_decode_paged: the paged cache instead of k/v_buf
+  const int32_t* block_table;
+  int32_t max_blocks, page, num_blocks, hkv_total, hkv_begin;
+};
+
 template <int D, bool F32>
 static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const void* q, int64_t q_row_stride,
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
-                        uint32_t* merge_ctr, cudaStream_t stream) {
+                        uint32_t* merge_ctr, cudaStream_t stream, const PagedSrc* paged = nullptr) {
   using C = AttnCfg<D, F32>;
   AttnParams p{};
   p.work_p = dp->prefill_work;
@@ -1158,10 +1180,27 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   const uint64_t dims[3] = {(uint64_t)D, (uint64_t)dp->buffer_tokens, (uint64_t)hkv_count};
   const uint64_t strides[2] = {(uint64_t)C::ROW_BYTES, (uint64_t)dp->buffer_tokens * C::ROW_BYTES};
   const uint32_t box[3] = {(uint32_t)C::ATOM_ELEMS, 128u, 1u};
-  pi_status s = encode_tmap_3d(&tmK, dt, k_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (s != PI_OK) return s;
-  s = encode_tmap_3d(&tmV, dt, v_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (s != PI_OK) return s;
+  pi_status s;
+  if (paged == nullptr) {
+    s = encode_tmap_3d(&tmK, dt, k_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != PI_OK) return s;
+    s = encode_tmap_3d(&tmV, dt, v_buf, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != PI_OK) return s;
+  } else {
+    // paged cache [blocks * page slots, hkv_total, d]: box (atom, 1 head, 128 slots) lands in smem
+    // exactly like a buffer tile (128 rows of 128 B, SWIZZLE_128B)
+    const uint64_t pdims[3] = {(uint64_t)D, (uint64_t)paged->hkv_total, (uint64_t)paged->num_blocks * paged->page};
+    const uint64_t pstrides[2] = {(uint64_t)C::ROW_BYTES, (uint64_t)paged->hkv_total * C::ROW_BYTES};
+    const uint32_t pbox[3] = {(uint32_t)C::ATOM_ELEMS, 1u, 128u};
+    s = encode_tmap_3d(&tmK, dt, k_buf, pdims, pstrides, pbox, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != PI_OK) return s;
+    s = encode_tmap_3d(&tmV, dt, v_buf, pdims, pstrides, pbox, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != PI_OK) return s;
+    p.block_table = paged->block_table;
+    p.max_blocks = paged->max_blocks;
+    p.page = paged->page;
+    p.kv_head0 = paged->hkv_begin;
+  }
   // Q as a 2D (row = token * q_heads_stride + head, d) tensor for tile::gather4 (box {atom, 1})
   CUtensorMap tmQ;
   p.q_heads_stride = (int32_t)(q_row_stride / D);
@@ -1186,7 +1225,8 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
                                  const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t gqa_ratio,
                                  int32_t head_dim, float softmax_scale, pi_dtype dt, void* out,
                                  int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
-                                 pi_stream_t stream, uint32_t* merge_ctr = nullptr, bool want_merge = false) {
+                                 pi_stream_t stream, uint32_t* merge_ctr = nullptr, bool want_merge = false,
+                                 const PagedSrc* paged = nullptr) {
   if (!dp) return fail(PI_EINVAL, "device plan is NULL");
   const bool decode = (mode & 2) && dp->n_decode_work > 0;
   const int32_t n_work = ((mode & 1) ? dp->n_prefill_work : 0) + ((mode & 2) ? dp->n_decode_work : 0);
@@ -1218,13 +1258,13 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dt == PI_BF16 && head_dim == 128)
     s = launch<128, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                           out_row_stride, lse, partial_o, partial_lse, merge_ctr, st);
+                           out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged);
   else if (dt == PI_BF16 && head_dim == 64)
     s = launch<64, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                          out_row_stride, lse, partial_o, partial_lse, merge_ctr, st);
+                          out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged);
   else
     s = launch<64, true>(dp, mode, false, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                         out_row_stride, lse, partial_o, partial_lse, merge_ctr, st);
+                         out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged);
   return s == PI_OK ? ok() : s;
 }
 
@@ -1260,6 +1300,24 @@ pi_status packinfer_attention(const pi_device_plan* dp, const void* q, int64_t q
                               float* partial_o, float* partial_lse, pi_stream_t stream) {
   return pi::attention_entry(3, dp, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, head_dim, softmax_scale,
                              dt, out, out_row_stride, lse, partial_o, partial_lse, stream);
+}
+
+pi_status packinfer_attention_decode_paged(const pi_device_plan* dp, const void* q, int64_t q_row_stride,
+                                          const void* k_paged, const void* v_paged, const int32_t* block_table,
+                                          int32_t max_blocks, int32_t page_size, int32_t num_blocks, int32_t hkv_total,
+                                          int32_t hkv_begin, int32_t hkv_count, int32_t gqa_ratio, int32_t head_dim,
+                                          float softmax_scale, pi_dtype dt, void* out, int64_t out_row_stride,
+                                          float* lse, float* partial_o, float* partial_lse, pi_stream_t stream) {
+  using namespace pi;
+  if (!dp) return fail(PI_EINVAL, "device plan is NULL");
+  if (dp->n_prefill_work > 0) return fail(PI_EINVAL, "paged decode needs a decode-only plan (PI_PLAN_PAGED)");
+  if (!block_table || max_blocks < 1 || num_blocks < 1) return fail(PI_EINVAL, "bad block table / num_blocks");
+  if (page_size < 128 || page_size % 128) return fail(PI_EINVAL, "page_size must be a multiple of 128");
+  if (hkv_begin < 0 || hkv_count < 1 || hkv_begin + hkv_count > hkv_total) return fail(PI_EINVAL, "bad KV head range");
+  if (dt == PI_FP32) return fail(PI_EUNSUP, "paged decode supports bf16 operands only");
+  const PagedSrc src{block_table, max_blocks, page_size, num_blocks, hkv_total, hkv_begin};
+  return attention_entry(2, dp, q, q_row_stride, k_paged, v_paged, hkv_count, gqa_ratio, head_dim, softmax_scale, dt,
+                         out, out_row_stride, lse, partial_o, partial_lse, stream, nullptr, false, &src);
 }
 
 pi_status packinfer_attention_merge(const pi_device_plan* dp, const void* q, int64_t q_row_stride, const void* k_buf,

@@ -68,6 +68,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const int64_t chunk = cfg->decode_chunk;
   const bool no_qpack = (cfg->flags & PI_PLAN_NO_QPACK) != 0;
   const bool dpack = (cfg->flags & PI_PLAN_DPACK) != 0;
+  const bool paged = (cfg->flags & PI_PLAN_PAGED) != 0;
   if (C < 1) return fail(PI_EINVAL, "capacity must be >= 1");
   if (delta < 0 || cfg->num_groups < 0 || cfg->mem_cap < 0)
     return fail(PI_EINVAL, "negative headroom / num_groups / mem_cap");
@@ -76,7 +77,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   if (TQ != 128 || TK != 128) return fail(PI_EINVAL, "tile_q and tile_k must be 128");
   if (chunk < TK || chunk % TK) return fail(PI_EINVAL, "decode_chunk must be a positive multiple of tile_k");
   if (r < 1 || r > 16) return fail(PI_EINVAL, "gqa_ratio must be in [1, 16]");
-  if (cfg->flags & ~(PI_PLAN_NO_QPACK | PI_PLAN_DPACK)) return fail(PI_EINVAL, "unknown pi_config.flags bits");
+  if (cfg->flags & ~(PI_PLAN_NO_QPACK | PI_PLAN_DPACK | PI_PLAN_PAGED))
+    return fail(PI_EINVAL, "unknown pi_config.flags bits");
   int64_t total_q = 0;
   for (int32_t i = 0; i < n; ++i) {
     const int32_t L = kv_len[i], q = q_len[i];
@@ -88,6 +90,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       return fail(PI_EINVAL, "prefix_len[" + std::to_string(p) + "] must be in [1, kv_len - q_len] of request " +
                                  std::to_string(i));
     total_q += q;
+    if ((cfg->flags & PI_PLAN_PAGED) && q != 1)
+      return fail(PI_EINVAL, "PI_PLAN_PAGED plans decode batches only (q_len == 1)");
   }
   if (total_q > INT32_MAX) return fail(PI_EINVAL, "total_q exceeds int32");
   // Decode-loop steps since the last consolidation: appended[i] new tokens of decode
@@ -461,7 +465,17 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
     }
     pack.clear();
   };
-  for (int32_t g = 0; g < G; ++g) {
+  // PI_PLAN_PAGED (NEXT-4 "no packed I/O" baseline, Fig. breakdown): decode items over
+  // each request's LOGICAL tokens [0, kv_len + appended) read straight from the paged cache
+  // (packinfer_attention_decode_paged): no consolidation, no prefix co-location; the block-table
+  // row rides in pi_work.reserved.  Chunk boundaries are multiples of tile_k, so with page_size
+  // a multiple of 128 a 128-key tile never crosses a page.
+  for (int32_t i = 0; paged && i < n; ++i) {
+    const int64_t b0 = (int64_t)dwork.size();
+    emit_decode(-1, &i, 1, 0, (int64_t)kv_len[i] + app(i));
+    for (int64_t w = b0; w < (int64_t)dwork.size(); ++w) dwork[w].reserved = i;
+  }
+  for (int32_t g = 0; !paged && g < G; ++g) {
     const auto& ent = entries[g];
     for (size_t a = 0; a < ent.size(); ++a) {
       const Entry& e = ent[a];

@@ -29,6 +29,7 @@ EXPORTS = [
     "packinfer_strerror", "packinfer_last_error", "packinfer_version", "packinfer_default_config",
     "packinfer_plan", "packinfer_plan_rows", "packinfer_plan_upload", "packinfer_relayout_kv",
     "packinfer_attention_prefill", "packinfer_attention_decode", "packinfer_attention", "packinfer_attention_merge",
+    "packinfer_attention_decode_paged",
     "packinfer_merge",
     "packinfer_plan_step", "packinfer_should_regroup", "packinfer_append_kv",
 ]
@@ -49,6 +50,7 @@ class pi_config(C.Structure):
 
 PI_PLAN_NO_QPACK = 1   # ablation: one Q tile set per request (include/packinfer.h)
 PI_PLAN_DPACK = 2      # option: pack short decode suffixes of a group into one decode item
+PI_PLAN_PAGED = 4      # ablation (NEXT-4): decode items over logical tokens, read from the paged cache
 
 
 PIECE_DT = np.dtype([("request", "<i4"), ("piece", "<i4"), ("kv_begin", "<i4"), ("kv_len", "<i4"), ("group", "<i4")])
@@ -141,6 +143,9 @@ def lib():
         L.packinfer_attention_merge.restype = C.c_int
         L.packinfer_attention_merge.argtypes = [C.POINTER(pi_device_plan), vp, i64, vp, vp, i32, i32, i32, f32, C.c_int,
                                                 vp, i64, vp, vp, vp, vp, vp]
+        L.packinfer_attention_decode_paged.restype = C.c_int
+        L.packinfer_attention_decode_paged.argtypes = [C.POINTER(pi_device_plan), vp, i64, vp, vp, vp, i32, i32, i32, i32,
+                                                       i32, i32, i32, i32, f32, C.c_int, vp, i64, vp, vp, vp, vp]
         L.packinfer_merge.restype = C.c_int
         L.packinfer_merge.argtypes = [C.POINTER(pi_device_plan), vp, vp, i32, i32, C.c_int, vp, i64, vp, vp]
         _lib = L
@@ -343,6 +348,24 @@ def packinfer_attention_merge(dp, q, k_buf, v_buf, out, lse, partial_o, partial_
                                            None if partial_lse is None else partial_lse.data_ptr(),
                                            None if merge_counters is None else merge_counters.data_ptr(),
                                            _stream_ptr(stream)), "packinfer_attention_merge")
+
+
+def packinfer_attention_decode_paged(dp, q, k_paged, v_paged, block_table, out, lse=None, partial_o=None,
+                                     partial_lse=None, gqa_ratio: int = 1, hkv_begin: int = 0,
+                                     hkv_count: Optional[int] = None, scale: float = 0.0, stream=None):
+    """NEXT-4 ablation: decode straight from the paged cache (plan made with PI_PLAN_PAGED)."""
+    import torch
+    nb, page, hkv_total, d = k_paged.shape
+    hkv_count = hkv_total - hkv_begin if hkv_count is None else hkv_count
+    dt = _dt(q)
+    if dt == PI_BF16 and out.dtype == torch.float32:
+        dt = PI_BF16_OUT_F32
+    _check(lib().packinfer_attention_decode_paged(
+        C.byref(dp), q.data_ptr(), q.stride(0), k_paged.data_ptr(), v_paged.data_ptr(), block_table.data_ptr(),
+        block_table.shape[1], page, nb, hkv_total, hkv_begin, hkv_count, gqa_ratio, d, float(scale), dt,
+        out.data_ptr(), out.stride(0), None if lse is None else lse.data_ptr(),
+        None if partial_o is None else partial_o.data_ptr(), None if partial_lse is None else partial_lse.data_ptr(),
+        _stream_ptr(stream)), "packinfer_attention_decode_paged")
 
 
 def packinfer_should_regroup(steps: int, drift: int, capacity: int) -> bool:

@@ -19,7 +19,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     syms = declared_symbols()
-    assert len(syms) == 16, syms
+    assert len(syms) == 17, syms
     L = pk.lib()
     for s in syms:
         assert hasattr(L, s), s

@@ -537,3 +537,39 @@ def test_packed_decode_items_option(seed):
     assert res[pk.PI_PLAN_DPACK][2] < res[0][2]
     ro, rl = H.oracle_full(b, t)
     H.compare(res[pk.PI_PLAN_DPACK][0], res[pk.PI_PLAN_DPACK][1], ro, rl)
+
+
+@pytest.mark.parametrize("name", ["small", "cfg4_decode"])
+def test_paged_decode_ablation(name):
+    """NEXT-4 "no packed I/O" ablation: a PI_PLAN_PAGED plan decoded straight from the paged cache
+    (packinfer_attention_decode_paged: no relayout, no prefix co-location) matches the oracle, as
+    does the packed path on the same batch; the packed plan reads fewer KV tokens when prefixes are
+    shared (Eq. 5)."""
+    from paper_2602_06072_b200 import packinfer as pk
+    if name == "small":
+        b = W.random_batch(811, n=14, max_len=2500, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    else:
+        b = W.make_batch(name)
+    t = W.make_tensors(b, device="cuda")
+    r = b.hq // b.hkv
+    pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16, "cuda",
+                        decode_chunk=512, flags=pk.PI_PLAN_PAGED)
+    out = torch.full((b.total_q, b.hq, b.d), float("nan"), dtype=torch.float32, device="cuda")
+    lse = torch.full((b.hq, b.total_q), float("nan"), dtype=torch.float32, device="cuda")
+    pk.packinfer_attention_decode_paged(pb.dp, t["q"], t["k_paged"], t["v_paged"], t["block_table"], out, lse,
+                                        pb.partial_o, pb.partial_lse, r)
+    pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, lse)
+    torch.cuda.synchronize()
+    if name == "small":
+        ro, rl = H.oracle_full(b, t)
+        H.compare(out, lse, ro, rl)
+    else:
+        rows = [(i, 0) for i in range(b.n)]
+        ro, rl = OA.attention_rows(t["q"].cpu(), t["k_paged"].cpu(), t["v_paged"].cpu(), t["block_table"].cpu(),
+                                   b.kv_len, b.q_len, b.page_size, rows)
+        err = np.abs(out.cpu().numpy() - ro)
+        assert err.max() <= H.ATOL_MAX and err.mean() <= H.ATOL_MEAN
+        assert np.abs(lse.cpu().numpy().T - rl).max() <= 1e-3
+        packed = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, pk.default_config(gqa_ratio=r))
+        paged_keys = int(sum(s["len"] for s in pb.plan.spans))
+        assert int(packed.c.copy_tokens) < paged_keys == int(b.kv_len.sum())
