@@ -2,17 +2,20 @@
 # Launch list + full ncu captures of the prefill / decode attention and relayout kernels
 # (run under gpurun, 1 GPU).  Usage: scripts/profile.sh <tag>
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 OUT=gpurun_out/prof_$TAG
 mkdir -p $OUT
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-  --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-mixed --no-loop > $OUT/launches_bench.log 2>&1
+B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-mixed --no-loop --no-prefix"
+# launch list of one short bench (kernel durations, cold-cache + serialised: shares, not absolutes)
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file $OUT/launches.csv $B > $OUT/launches_bench.log 2>&1
+# prefill: the 2nd attention launch of the headline (timed step); decode: the 2nd of the cfg3 section
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 1 -c 1 \
-  -o $OUT/prefill python bench.py --steps 1 --warmup 1 --no-decode --no-e2e --no-cpu --no-mixed --no-loop > $OUT/prefill.log 2>&1
+  -o $OUT/prefill $B --no-decode > $OUT/prefill.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 3 -c 1 \
-  -o $OUT/decode python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-mixed --no-loop > $OUT/decode.log 2>&1
+  -o $OUT/decode $B > $OUT/decode.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:relayout -s 1 -c 1 \
-  -o $OUT/relayout python bench.py --steps 1 --warmup 1 --no-decode --no-e2e --no-cpu --no-mixed --no-loop > $OUT/relayout.log 2>&1
+  -o $OUT/relayout $B --no-decode > $OUT/relayout.log 2>&1
 for k in prefill decode relayout; do
   ncu -i $OUT/$k.ncu-rep --page raw --csv > $OUT/${k}_raw.csv 2>/dev/null
 done
