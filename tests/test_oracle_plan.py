@@ -350,3 +350,21 @@ def test_greedy_step_replay(seed):
         if pc.prefix >= 0:
             held[g].add(pc.prefix)
     assert loads == [grp.load for grp in pl.groups]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_valid_pairs_count_brute_force(seed):
+    """oracle.plan.valid_pairs_count (reading R11: causal within a request, block-diagonal across
+    requests) against enumerating every (query, key) pair of tiny batches, plus the closed forms
+    L(L+1)/2 (full prefill) and L (one decode row)."""
+    rng = np.random.default_rng(seed)
+    kv = rng.integers(1, 40, size=6)
+    q = np.array([int(rng.integers(1, L + 1)) for L in kv])
+    brute = 0
+    for L, ql in zip(kv.tolist(), q.tolist()):
+        for t in range(ql):
+            pos = L - ql + t
+            brute += sum(1 for key in range(L) if key <= pos)
+    assert P.valid_pairs_count(kv, q) == brute
+    assert P.valid_pairs_count([37], [37]) == 37 * 38 // 2
+    assert P.valid_pairs_count([37], [1]) == 37
