@@ -185,7 +185,10 @@ typedef struct {
   int64_t appended_total;
   void* arena;  size_t arena_bytes;        /* the host arena holding every table          */
   size_t rows_offset;                      /* byte offset of the row table in the DEVICE arena */
-  size_t device_arena_bytes;               /* device arena size: host tables + row table      */
+  size_t sched_offset;                     /* byte offset of the attention launches' dynamic
+                                              scheduler counter in the DEVICE arena            */
+  size_t device_arena_bytes;               /* device arena size: host tables + row table +
+                                              scheduler counter                               */
 } pi_plan;
 
 /* Alg. 1 Parts 1-2 plus the packed execution domain.
@@ -232,6 +235,9 @@ typedef struct {
   const int32_t* append_pos;                 /* [n_requests] (see pi_plan)                      */
   const int32_t* slot_merge;                 /* [n_partial_slots] (see pi_plan); NULL disables
                                                 packinfer_attention_merge                        */
+  uint32_t* sched;                           /* dynamic unit counter of the attention launches:
+                                                each launch resets it on its stream, so one
+                                                attention launch per device plan at a time      */
 } pi_device_plan;
 
 /* Enqueue one host->device copy of plan->arena (arena_bytes) into dev_arena (device, >=

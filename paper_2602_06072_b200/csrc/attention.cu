@@ -47,6 +47,9 @@
 #ifndef PI_P_ROUNDED_SUM
 #define PI_P_ROUNDED_SUM 2   // O normalised by the row sum of the bf16-rounded P: 1 = FHADD.BF16, 2 = PRMT + FADD2; 0 = exact sum
 #endif
+#ifndef PI_DYN_SCHED
+#define PI_DYN_SCHED 1   // dynamic LPT list scheduling of units (0: static snake order, A/B)
+#endif
 #ifndef PI_MERGE_ATOM
 #define PI_MERGE_ATOM 0   // merge counters: 0 atom.release, 1 atom.acq_rel, 2 one fence per unit + relaxed, 3 relaxed (A/B)
 #endif
@@ -99,6 +102,7 @@ struct AttnParams {
   // paged mode (packinfer_attention_decode_paged): K/V tiles straight from the paged cache
   const int32_t* block_table;   // NULL = group-contiguous buffers
   int32_t max_blocks, page, kv_head0;
+  uint32_t* sched;              // dynamic unit counter (zeroed before the launch)
 };
 
 // One paged-mode tile: logical keys [k0, k0 + 128) of block-table row `row` = 128 consecutive slots
@@ -176,7 +180,8 @@ struct AttnCfg {
 enum BarId {
   B_QFULL = 0, B_QFREE, B_KFULL0, B_KFULL1, B_KFREE0, B_KFREE1, B_VFULL0, B_VFULL1, B_VFREE0, B_VFREE1,
   B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
-  B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_EFULL0, B_EFREE0 = B_EFULL0 + 4, B_COUNT = B_EFREE0 + 4
+  B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_EFULL0, B_EFREE0 = B_EFULL0 + 4, B_UFULL0 = B_EFREE0 + 4,
+  B_UFREE0 = B_UFULL0 + 8, B_COUNT = B_UFREE0 + 8
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
@@ -202,10 +207,22 @@ struct Unit {
   bool has_b;
 };
 
-// Static LPT schedule: units are sorted by cost (descending); round k hands CTA b the unit
-// k*G + b on even rounds and k*G + (G-1-b) on odd rounds ("snake"), which keeps per-CTA totals
-// within ~1% on the BASELINE.json batches without any inter-CTA communication.
-__device__ __forceinline__ int snake_unit(int k, int b, int G) { return k * G + ((k & 1) ? (G - 1 - b) : b); }
+// Dynamic LPT schedule: units are sorted by cost (descending); CTA b starts with unit b and then
+// takes the next unsorted unit from one global counter whenever its producer warp starts a unit
+// (list scheduling of an LPT-sorted list: within ~1-8 % of the mean per-CTA load even when a KV-head
+// shard leaves only ~6 units per CTA, where a static snake order left up to 53 %).  The producer
+// publishes the sequence through an 8-deep smem ring (full / free mbarriers) that every other role
+// warp reads in order; -1 ends it.
+constexpr int kUnitRing = 8;
+constexpr int kUnitConsumers = 11;   // MMA issuer, Q gather, warp 3, 8 softmax warps (one arrive each)
+
+__device__ __forceinline__ int ring_get(const int* ring, uint64_t* bar, int k) {
+  mbar_wait(&bar[B_UFULL0 + (k & (kUnitRing - 1))], (k / kUnitRing) & 1);
+  return ring[k & (kUnitRing - 1)];
+}
+__device__ __forceinline__ void ring_release(uint64_t* bar, int k, int lane) {
+  if (lane == 0) mbar_arrive(&bar[B_UFREE0 + (k & (kUnitRing - 1))]);
+}
 
 // Unit w: prefill units first (each list is sorted by cost, descending), then decode units, so
 // the cheap decode units fill the tail of the one persistent launch (NEXT-3).
@@ -248,6 +265,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * B_COUNT);
+  int* uring = reinterpret_cast<int*>(smem + C::OFF_BAR + 8 * B_COUNT + 16);   // unit ring (kUnitRing)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -266,6 +284,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       mbar_init(&bar[B_PVH0 + s], 1);
       mbar_init(&bar[B_OFULL0 + s], 1);
       mbar_init(&bar[B_OFREE0 + s], 128);
+    }
+    for (int s = 0; s < kUnitRing; ++s) {   // unit ring: producer -> every consumer warp
+      mbar_init(&bar[B_UFULL0 + s], 1);
+      mbar_init(&bar[B_UFREE0 + s], kUnitConsumers);
     }
     for (int s = 0; s < 4; ++s) {   // merge hand-off ring (4 deep)
       mbar_init(&bar[B_EFULL0 + s], 256);   // all softmax threads stored a single unit's partials
@@ -293,21 +315,35 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // The whole warp walks the schedule (uniform values); one elected lane issues each copy.
     uint32_t t = 0;
     // next unit's work item + first span loaded one unit ahead (as in the softmax warps)
-    Unit nu;
-    pi_span nsp = {0, 0};
-    if ((int)blockIdx.x < total) {
-      nu = get_unit<UK>(p, blockIdx.x);
-      nsp = p.spans[nu.wk.span_begin];
-    }
-    for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+    // publish unit k of this CTA into the ring (waits until every consumer read slot k - ring)
+    auto ring_put = [&](int k, int wv) {
+      mbar_wait(&bar[B_UFREE0 + (k & (kUnitRing - 1))], ((k / kUnitRing) & 1) ^ 1);
+      if (lane == 0) {
+        uring[k & (kUnitRing - 1)] = wv;
+        mbar_arrive(&bar[B_UFULL0 + (k & (kUnitRing - 1))]);
+      }
+      __syncwarp();
+    };
+    int w = blockIdx.x;   // grid <= total units
+    ring_put(0, w);
+    Unit nu = get_unit<UK>(p, w);
+    pi_span nsp = p.spans[nu.wk.span_begin];
+    for (int k = 0; w >= 0; ++k) {
       const Unit u = nu;
       const pi_span span0 = nsp;
-      {
-        const int wn = snake_unit(k + 1, blockIdx.x, gridDim.x);
-        if (wn < total) {
-          nu = get_unit<UK>(p, wn);
-          nsp = p.spans[nu.wk.span_begin];
-        }
+      int wn = 0;
+      if (PI_DYN_SCHED) {
+        if (lane == 0) wn = (int)atomicAdd(p.sched, 1u) + (int)gridDim.x;
+        wn = __shfl_sync(0xffffffffu, wn, 0);
+      } else {   // A/B: static "snake" order (round k: k G + b, or k G + G - 1 - b on odd rounds)
+        const int r = k + 1;
+        wn = r * (int)gridDim.x + ((r & 1) ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x);
+      }
+      if (wn >= total) wn = -1;
+      ring_put(k + 1, wn);
+      if (wn >= 0) {
+        nu = get_unit<UK>(p, wn);
+        nsp = p.spans[nu.wk.span_begin];
       }
       for (int s = 0; s < u.wk.span_count; ++s) {
         const pi_span sp = s == 0 ? span0 : p.spans[u.wk.span_begin + s];
@@ -342,6 +378,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           }
         }
       }
+      w = wn;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
@@ -413,14 +450,13 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         }
         __syncwarp();
       };
-      Unit nu;
-      if ((int)blockIdx.x < total) nu = get_unit<UK>(p, blockIdx.x);
-      for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+      int w = ring_get(uring, bar, 0);
+      Unit nu = get_unit<UK>(p, w);
+      for (int k = 0; w >= 0; ++k) {
         const Unit u = nu;   // loaded one unit ahead
-        {
-          const int wn = snake_unit(k + 1, blockIdx.x, gridDim.x);
-          if (wn < total) nu = get_unit<UK>(p, wn);
-        }
+        const int wn = ring_get(uring, bar, k + 1);
+        ring_release(bar, k, lane);
+        if (wn >= 0) nu = get_unit<UK>(p, wn);
         const int n = u.wk.n_ktiles;
         trace_unit(p, item, 0);
         mbar_wait(&bar[B_QFULL], item & 1);
@@ -522,6 +558,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         trace_unit(p, item, 3);
         t += n;
         ++item;
+        w = wn;
       }
     }
     __syncwarp();
@@ -531,7 +568,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     // Q rows are addressed through the plan's row table: lane g gathers rows 4g..4g+3 of each tile
     // (one gather4 per 128-byte atom column) straight into the SWIZZLE_128B K-major operand layout.
     uint32_t item = 0;
-    for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+    for (int k = 0, w = ring_get(uring, bar, 0); w >= 0; ++k, w = ring_get(uring, bar, k)) {
+      ring_release(bar, k, lane);
       const Unit u = get_unit<UK>(p, w);
       const int nt = u.has_b ? 2 : 1;
       trace_unit(p, item, 4);
@@ -573,7 +611,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       // the same order, so outputs are bitwise equal to the separate merge - and re-zeroes the
       // counter for the next launch.
       uint32_t epi = 0;
-      for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+      for (int k = 0, w = ring_get(uring, bar, 0); w >= 0; ++k, w = ring_get(uring, bar, k)) {
+        ring_release(bar, k, lane);
         const Unit u = get_unit<UK>(p, w);
         if (u.has_b) continue;
         const uint32_t e = epi & 3;
@@ -666,9 +705,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         ++epi;
       }
     }
-    if constexpr (F32) {
+    else if constexpr (F32) {
       uint32_t t = 0;
-      for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+      for (int k = 0, w = ring_get(uring, bar, 0); w >= 0; ++k, w = ring_get(uring, bar, k)) {
+        ring_release(bar, k, lane);
         const Unit u = get_unit<UK>(p, w);
         const float* vsrc = reinterpret_cast<const float*>(p.v_buf) + (int64_t)u.kvh * p.buffer_tokens * D;
         for (int s = 0; s < u.wk.span_count; ++s) {
@@ -696,6 +736,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           }
         }
       }
+    } else {
+      // nothing to do for this launch: still consume the unit ring (one reader per slot expected)
+      for (int k = 0, w = ring_get(uring, bar, 0); w >= 0; ++k, w = ring_get(uring, bar, k)) ring_release(bar, k, lane);
     }
   } else {
     // ------------------------------------------------------------------ softmax / epilogue
@@ -737,15 +780,15 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       nrow = row_id < nu.wk.row_count ? p.rows[nu.wk.row_begin + row_id] : pi_row{0, 0, 0, 0};
       nsp = p.spans[nu.wk.span_begin];
     };
-    if ((int)blockIdx.x < total) prefetch(blockIdx.x);
-    for (int k = 0, w = blockIdx.x; w < total; ++k, w = snake_unit(k, blockIdx.x, gridDim.x)) {
+    int w = ring_get(uring, bar, 0);
+    prefetch(w);
+    for (int k = 0; w >= 0; ++k) {
       const Unit u = nu;
       const pi_row row_pf = nrow;
       const pi_span span0 = nsp;
-      {
-        const int wn = snake_unit(k + 1, blockIdx.x, gridDim.x);
-        if (wn < total) prefetch(wn);
-      }
+      const int wn = ring_get(uring, bar, k + 1);
+      ring_release(bar, k, lane);
+      if (wn >= 0) prefetch(wn);
       const pi_work& wk = u.wk;
       const int n = wk.n_ktiles;
       // pair units: warpgroup X owns tile X (both key halves); single-tile units: warpgroup X owns
@@ -1102,6 +1145,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       if (u.has_b) pvh += n;   // PVH completes for pair units only
       t += n;
       ++ix;
+      w = wn;
     }
   }
   tc_fence_before();
@@ -1170,6 +1214,7 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   p.out_f32 = out_f32 ? 1 : 0;
   p.buffer_tokens = dp->buffer_tokens;
   p.trace = g_debug_trace;
+  p.sched = dp->sched;
   p.merges = dp->merges;
   p.slot_merge = dp->slot_merge;
   // fp32 operands: warp 3 stages V^T, so the entry point merges with a separate launch instead
@@ -1212,6 +1257,9 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
 
   const int64_t total = (int64_t)p.total_p + (int64_t)p.n_work_d * p.units_d;
   const int grid = (int)std::min<int64_t>(total, num_sms());
+  if (p.sched == nullptr) return fail(PI_EINVAL, "device plan has no scheduler counter (packinfer_plan_upload)");
+  s = cuda_check(cudaMemsetAsync(p.sched, 0, sizeof(uint32_t), stream), "scheduler counter reset");
+  if (s != PI_OK) return s;
   // kernel instance by the unit kinds present (see get_unit): a prefill-only launch with even r
   // has pair units only, a decode-only launch (or fp32 operands) single-tile units only
   const bool pairs_only = !F32 && p.n_work_d == 0 && (r % 2) == 0;

@@ -596,7 +596,8 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   const size_t need = std::max<size_t>(off, 256);
   // device arena = the host arena's tables + the expanded row table behind them
   const size_t o_rows = need;
-  const size_t dev_need = align_up(o_rows + sizeof(pi_row) * (size_t)n_rows, 256);
+  const size_t o_sched = align_up(o_rows + sizeof(pi_row) * (size_t)n_rows, 256);
+  const size_t dev_need = o_sched + 256;
 
   std::memset(out, 0, sizeof(*out));
   out->n_pieces = NP;
@@ -608,6 +609,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   out->n_rows = n_rows;
   out->n_segs = (int32_t)segs.size();
   out->rows_offset = o_rows;
+  out->sched_offset = o_sched;
   out->device_arena_bytes = dev_need;
   out->n_spans = (int32_t)spans.size();
   out->n_merges = (int32_t)merges.size();

@@ -67,6 +67,7 @@ extern "C" pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, si
   out->n_partial_slots = p->n_partial_slots;
   out->append_pos = static_cast<const int32_t*>(dev(p->append_pos));
   out->slot_merge = static_cast<const int32_t*>(dev(p->slot_merge));
+  out->sched = reinterpret_cast<uint32_t*>(D + p->sched_offset);
   out->buffer_tokens = p->buffer_tokens;
   out->n_requests = p->n_requests;
   out->total_q = p->total_q;

@@ -86,7 +86,7 @@ class pi_plan(C.Structure):
                 ("discrepancy", C.c_int32), ("reserved", C.c_int32),
                 ("append_pos", C.c_void_p), ("drift", C.c_int64), ("appended_total", C.c_int64),
                 ("arena", C.c_void_p), ("arena_bytes", C.c_size_t),
-                ("rows_offset", C.c_size_t), ("device_arena_bytes", C.c_size_t)]
+                ("rows_offset", C.c_size_t), ("sched_offset", C.c_size_t), ("device_arena_bytes", C.c_size_t)]
 
 
 class pi_device_plan(C.Structure):
@@ -98,7 +98,8 @@ class pi_device_plan(C.Structure):
                 ("merges", C.c_void_p), ("n_merges", C.c_int32), ("n_partial_slots", C.c_int32),
                 ("buffer_tokens", C.c_int64),
                 ("n_requests", C.c_int32), ("total_q", C.c_int32), ("gqa_ratio", C.c_int32),
-                ("tile_k", C.c_int32), ("append_pos", C.c_void_p), ("slot_merge", C.c_void_p)]
+                ("tile_k", C.c_int32), ("append_pos", C.c_void_p), ("slot_merge", C.c_void_p),
+                ("sched", C.c_void_p)]
 
 
 _lib = None
