@@ -114,7 +114,7 @@ __device__ __forceinline__ int paged_token(const AttnParams& p, int row, int k0)
 }
 
 // Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
-constexpr int TRACE_TILES = 64;
+constexpr int TRACE_TILES = 128;
 // Compiled in only with -DPI_TRACE=1 (scripts/trace_*.py build such a variant): the hot loops of
 // the production build carry no trace checks.
 #ifndef PI_TRACE
@@ -124,11 +124,11 @@ __device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int
   if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
     p.trace[tile * 24 + ev] = clock64();
 }
-// Per-unit events: trace[1536 + unit * 16 + ev], first 64 units of CTA 0 (0-3 MMA issuer, 4-6 Q
+// Per-unit events: trace[TRACE_TILES * 24 + unit * 16 + ev], first 64 units of CTA 0 (0-3 MMA issuer, 4-6 Q
 // gather, 7-11 softmax warp 4: unit start, first S landed, epilogue start (O landed), O read,
 // epilogue done).
 __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
-  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[64 * 24 + unit * 16 + ev] = clock64();
+  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[TRACE_TILES * 24 + unit * 16 + ev] = clock64();
 }
 
 template <int D, bool F32>
