@@ -131,7 +131,11 @@ __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, i
   if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[TRACE_TILES * 24 + unit * 16 + ev] = clock64();
 }
 
-template <int D, bool F32>
+#ifndef PI_DEC_NSV
+#define PI_DEC_NSV 3   // V stages of decode-only (single-tile) launches: V is held until P.V
+#endif
+
+template <int D, bool F32, int UK = 3>
 struct AttnCfg {
   static constexpr int ES = F32 ? 4 : 2;
   static constexpr int ROW_BYTES = D * ES;            // one Q/K/V row
@@ -139,14 +143,19 @@ struct AttnCfg {
   static constexpr int ATOM_ELEMS = 128 / ES;
   static constexpr int ATOM_BYTES = 128 * 128;        // one atom column of 128 rows
   static constexpr int TILE_BYTES = 128 * ROW_BYTES;  // 128 rows
-  static constexpr int NS = 2;                        // K/V pipeline stages
+  // K / V pipeline stages.  V tiles live until their P.V, K tiles only until S: decode-only
+  // launches (one Q tile) spend the second Q tile's space on a third V stage, so the producer runs
+  // one more tile ahead across unit boundaries.
+  static constexpr int NQ = UK == 2 ? 1 : 2;          // Q tiles resident
+  static constexpr int NSK = 2;
+  static constexpr int NSV = (UK == 2 && !F32) ? PI_DEC_NSV : 2;
   static constexpr int QK_STEPS = ROW_BYTES / 32;     // MMAs per S tile (32 bytes of K each)
   static constexpr int PV_STEPS = 128 * ES / 32;      // MMAs per O update (32 bytes of keys each)
   static constexpr int KEYS_PER_PV_STEP = 32 / ES;
   static constexpr int OFF_Q = 0;                     // Q_A, Q_B
-  static constexpr int OFF_K = 2 * TILE_BYTES;
-  static constexpr int OFF_V = OFF_K + NS * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_V + NS * TILE_BYTES;
+  static constexpr int OFF_K = NQ * TILE_BYTES;
+  static constexpr int OFF_V = OFF_K + NSK * TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_V + NSV * TILE_BYTES;
   static constexpr int OFF_XCH = OFF_BAR + 512;       // single units: (m, l, l_rounded) of both warpgroups
   static constexpr int SMEM = OFF_XCH + 2 * 128 * 16 + 1024;  // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
@@ -178,8 +187,8 @@ struct AttnCfg {
 // rescale (compute-sanitizer synccheck reports its unwaited phases; the waiter computes the parity
 // of the phase it needs, which cannot be overtaken: PV(j+1) needs this warpgroup's P(j+1)).
 enum BarId {
-  B_QFULL = 0, B_QFREE, B_KFULL0, B_KFULL1, B_KFREE0, B_KFREE1, B_VFULL0, B_VFULL1, B_VFREE0, B_VFREE1,
-  B_SF00, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
+  B_QFULL = 0, B_QFREE, B_KFULL0, B_KFREE0 = B_KFULL0 + 2, B_VFULL0 = B_KFREE0 + 2, B_VFREE0 = B_VFULL0 + 3,
+  B_SF00 = B_VFREE0 + 3, B_SF01, B_SF10, B_SF11, B_PHALF0, B_PHALF1, B_PFULL0, B_PFULL1, B_PVH0, B_PVH1,
   B_OFULL0, B_OFULL1, B_OFREE0, B_OFREE1, B_EFULL0, B_EFREE0 = B_EFULL0 + 4, B_UFULL0 = B_EFREE0 + 4,
   B_UFREE0 = B_UFULL0 + 8, B_COUNT = B_UFREE0 + 8
 };
@@ -255,10 +264,10 @@ __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
 }
 
 template <int D, bool F32, int UK>
-__global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
+__global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
     packed_attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ) {
-  using C = AttnCfg<D, F32>;
+  using C = AttnCfg<D, F32, UK>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -275,8 +284,6 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar[B_KFULL0 + s], 1);
       mbar_init(&bar[B_KFREE0 + s], 1);
-      mbar_init(&bar[B_VFULL0 + s], F32 ? 32 : 1);
-      mbar_init(&bar[B_VFREE0 + s], 1);
       mbar_init(&bar[B_SF00 + 2 * s], 1);
       mbar_init(&bar[B_SF00 + 2 * s + 1], 1);
       mbar_init(&bar[B_PHALF0 + s], 128);
@@ -284,6 +291,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       mbar_init(&bar[B_PVH0 + s], 1);
       mbar_init(&bar[B_OFULL0 + s], 1);
       mbar_init(&bar[B_OFREE0 + s], 128);
+    }
+    for (int s = 0; s < 3; ++s) {   // V stages (up to 3)
+      mbar_init(&bar[B_VFULL0 + s], F32 ? 32 : 1);
+      mbar_init(&bar[B_VFREE0 + s], 1);
     }
     for (int s = 0; s < kUnitRing; ++s) {   // unit ring: producer -> every consumer warp
       mbar_init(&bar[B_UFULL0 + s], 1);
@@ -348,8 +359,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       for (int s = 0; s < u.wk.span_count; ++s) {
         const pi_span sp = s == 0 ? span0 : p.spans[u.wk.span_begin + s];
         for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
-          const int st = t % C::NS;
-          const uint32_t ph = (t / C::NS) & 1;
+          const int st = t % C::NSK, sv = t % C::NSV;
+          const uint32_t ph = (t / C::NSK) & 1, phv = (t / C::NSV) & 1;
           // coordinates: buffers (d, token, kv head); paged cache (d, kv head, page slot)
           int c1 = k0, c2 = u.kvh;
           if (p.block_table != nullptr) {
@@ -366,12 +377,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           }
           __syncwarp();
           if constexpr (!F32) {
-            mbar_wait(&bar[B_VFREE0 + st], ph ^ 1);
+            mbar_wait(&bar[B_VFREE0 + sv], phv ^ 1);
             if (elect_one()) {
-              mbar_arrive_expect_tx(&bar[B_VFULL0 + st], C::TILE_BYTES);
+              mbar_arrive_expect_tx(&bar[B_VFULL0 + sv], C::TILE_BYTES);
 #pragma unroll
               for (int a = 0; a < C::ATOMS; ++a)
-                tma_load_3d(smem + C::OFF_V + st * C::TILE_BYTES + a * C::ATOM_BYTES, &tmV, &bar[B_VFULL0 + st],
+                tma_load_3d(smem + C::OFF_V + sv * C::TILE_BYTES + a * C::ATOM_BYTES, &tmV, &bar[B_VFULL0 + sv],
                             a * C::ATOM_ELEMS, c1, c2);
             }
             __syncwarp();
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       // softmax can start on the first half while the second is computed.
       auto issue_s = [&](int X, int b, uint32_t tt) {
         const uint64_t aq = dq + X * TILE16;
-        const uint64_t bk = dk + (tt % C::NS) * TILE16;
+        const uint64_t bk = dk + (tt % C::NSK) * TILE16;
         const uint32_t d_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
         if (elect_one()) {
 #pragma unroll
@@ -418,7 +429,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       // S(X) = Q_X K(tt)^T as one N = 128 chain into S/P region X; commits SF[X][0]
       auto issue_s_full = [&](int X, uint32_t tt) {
         const uint64_t aq = dq + X * TILE16;
-        const uint64_t bk = dk + (tt % C::NS) * TILE16;
+        const uint64_t bk = dk + (tt % C::NSK) * TILE16;
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < C::QK_STEPS; ++kk) {
@@ -436,7 +447,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
       // O_X += P_h V(tt)[keys 64h .. 64h+63]; P_h (this half's P) starts at TMEM column p_col;
       // first: overwrite O_X instead of accumulating
       auto issue_pv = [&](int X, uint32_t p_col, uint32_t tt, bool first, int h) {
-        const uint64_t bv = dv + (tt % C::NS) * TILE16;
+        const uint64_t bv = dv + (tt % C::NSV) * TILE16;
         const uint32_t p_tmem = tmem + p_col;
         const uint32_t d_tmem = tmem + (X ? C::TM_O1 : C::TM_O0);
         if (elect_one()) {
@@ -461,7 +472,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         trace_unit(p, item, 0);
         mbar_wait(&bar[B_QFULL], item & 1);
         trace_unit(p, item, 1);
-        mbar_wait(&bar[B_KFULL0 + (t % C::NS)], (t / C::NS) & 1);
+        mbar_wait(&bar[B_KFULL0 + (t % C::NSK)], (t / C::NSK) & 1);
         trace_unit(p, item, 2);
         tc_fence_after();
         if (u.has_b) {
@@ -470,7 +481,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
           // of 32 cycles), P overwrites S's first 64 columns, S(j+1) follows P(j).V in the in-order pipe.
           issue_s_full(0, t);
           issue_s_full(1, t);
-          commit(B_KFREE0 + (t % C::NS));
+          commit(B_KFREE0 + (t % C::NSK));
           if (n == 1) commit(B_QFREE);
           for (int j = 0; j < n; ++j) {
             const uint32_t tt = t + j;
@@ -478,7 +489,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               trace_ev(p, tt, 0 + 3 * X);
               mbar_wait(&bar[B_PHALF0 + X], (cnt[X] + j) & 1);
               trace_ev(p, tt, 1 + 3 * X);
-              if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
+              if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NSV)], (tt / C::NSV) & 1);
               if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
               tc_fence_after();
               issue_pv(X, X ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
@@ -487,18 +498,18 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
               tc_fence_after();
               issue_pv(X, (X ? C::TM_S1 : C::TM_S0) + 32, tt, false, 1);
               trace_ev(p, tt, 14 + X);
-              if (X == 1) commit(B_VFREE0 + (tt % C::NS));
+              if (X == 1) commit(B_VFREE0 + (tt % C::NSV));
               if (j == n - 1) {
                 commit(B_OFULL0 + X);
               } else {
                 if (X == 0) {
-                  mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NS)], ((tt + 1) / C::NS) & 1);
+                  mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NSK)], ((tt + 1) / C::NSK) & 1);
                   tc_fence_after();
                 }
                 issue_s_full(X, tt + 1);
                 trace_ev(p, tt, 2 + 3 * X);
                 if (X == 1) {
-                  commit(B_KFREE0 + ((tt + 1) % C::NS));
+                  commit(B_KFREE0 + ((tt + 1) % C::NSK));
                   if (j + 1 == n - 1) commit(B_QFREE);
                 }
               }
@@ -511,12 +522,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         } else {
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
           issue_s(0, 0, t);
-          commit(B_KFREE0 + (t % C::NS));
+          commit(B_KFREE0 + (t % C::NSK));
           if (n > 1) {
-            mbar_wait(&bar[B_KFULL0 + ((t + 1) % C::NS)], ((t + 1) / C::NS) & 1);
+            mbar_wait(&bar[B_KFULL0 + ((t + 1) % C::NSK)], ((t + 1) / C::NSK) & 1);
             tc_fence_after();
             issue_s(0, 1, t + 1);
-            commit(B_KFREE0 + ((t + 1) % C::NS));
+            commit(B_KFREE0 + ((t + 1) % C::NSK));
           }
           if (n <= 2) commit(B_QFREE);
           for (int j = 0; j < n; ++j) {
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             trace_ev(p, tt, 0);
             mbar_wait(&bar[B_PHALF0 + b], (cnt[b] + (j >> 1)) & 1);
             trace_ev(p, tt, 1);
-            mbar_wait(&bar[B_VFULL0 + (tt % C::NS)], (tt / C::NS) & 1);
+            mbar_wait(&bar[B_VFULL0 + (tt % C::NSV)], (tt / C::NSV) & 1);
             if (j == 0) {
               mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
               mbar_wait(&bar[B_OFREE1], (ix[1] & 1) ^ 1);
@@ -537,16 +548,16 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
             mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
             tc_fence_after();
             issue_pv(1, (b ? C::TM_S1 : C::TM_S0) + C::P1_SINGLE, tt, j == 0, 1);
-            commit(B_VFREE0 + (tt % C::NS));
+            commit(B_VFREE0 + (tt % C::NSV));
             if (j == n - 1) {
               commit(B_OFULL0);
               commit(B_OFULL1);
             }
             if (j + 2 < n) {
-              mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NS)], ((tt + 2) / C::NS) & 1);
+              mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NSK)], ((tt + 2) / C::NSK) & 1);
               tc_fence_after();
               issue_s(0, b, tt + 2);
-              commit(B_KFREE0 + ((tt + 2) % C::NS));
+              commit(B_KFREE0 + ((tt + 2) % C::NSK));
               if (j + 2 == n - 1) commit(B_QFREE);
             }
           }
@@ -714,8 +725,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
         for (int s = 0; s < u.wk.span_count; ++s) {
           const pi_span sp = p.spans[u.wk.span_begin + s];
           for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
-            const int st = t % C::NS;
-            mbar_wait(&bar[B_VFREE0 + st], ((t / C::NS) & 1) ^ 1);
+            const int st = t % C::NSV;
+            mbar_wait(&bar[B_VFREE0 + st], ((t / C::NSV) & 1) ^ 1);
             uint8_t* vt = smem + C::OFF_V + st * C::TILE_BYTES;
             for (int idx = lane; idx < 128 * (D / 4); idx += 32) {
               const int key = idx / (D / 4), c4 = idx % (D / 4);
@@ -951,7 +962,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32>::THREADS, 1)
                     // tcgen05 pipe); single-tile units issue it after S(j), so wait
                     if (!u.has_b) {
                       const uint32_t tp = t + j - 1;
-                      mbar_wait(&bar[B_VFREE0 + (tp % C::NS)], (tp / C::NS) & 1);
+                      mbar_wait(&bar[B_VFREE0 + (tp % C::NSV)], (tp / C::NSV) & 1);
                       tc_fence_after();
                     }
                     rescale_o(alpha);
@@ -1161,7 +1172,7 @@ unsigned long long* g_debug_trace = nullptr;
 template <int D, bool F32, int UK>
 static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                const CUtensorMap& tmQ, int grid, cudaStream_t stream) {
-  using C = AttnCfg<D, F32>;
+  using C = AttnCfg<D, F32, UK>;
   if constexpr (F32 && UK != 2) {
     return fail(PI_EUNSUP, "fp32 operands run single-tile units only");
   } else {
@@ -1185,7 +1196,7 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                         uint32_t* merge_ctr, cudaStream_t stream, const PagedSrc* paged = nullptr) {
-  using C = AttnCfg<D, F32>;
+  using C = AttnCfg<D, F32>;   // tile geometry only (independent of the unit kinds)
   AttnParams p{};
   p.work_p = dp->prefill_work;
   p.work_d = dp->decode_work;
