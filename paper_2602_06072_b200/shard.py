@@ -178,8 +178,8 @@ def rank_tables(host_plan, owner, rank: int):
     return {"work": work_all[keep_w], "copies": my_copies,
             "prefix": np.concatenate([[0], np.cumsum(my_ext)]).astype(np.int64),
             "copy_tokens": int(my_copies["len"].sum()) if len(my_copies) else 0,
-            "rows": rows, "merges": merges_r, "n_cross_slots": n_cross_slots,
-            "n_cross_rows": len(cross), "owned_tokens": owned_tokens}
+            "rows": rows, "merges": merges_r, "n_cross_slots": int(n_cross_slots),
+            "n_cross_rows": len(cross), "owned_tokens": [int(x) for x in owned_tokens]}
 
 
 class RankPlan:
@@ -225,7 +225,7 @@ class RankPlan:
         self.n_work = len(tb["work"])
         self.ktiles = int(tb["work"]["n_ktiles"].sum()) if len(tb["work"]) else 0
         hq, d = batch.hkv * batch.r, batch.d
-        self.exchange_bytes = self.n_cross_slots * hq * (d + 1) * 4
+        self.exchange_bytes = int(self.n_cross_slots * hq * (d + 1) * 4)
 
     def relayout_cells(self) -> int:
         return self.cells

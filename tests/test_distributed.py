@@ -211,3 +211,18 @@ def test_rank_tables_split_row_exchange(world):
                 g = int(np.searchsorted(bases, lo, side="right")) - 1
                 assert owner[g] != r or lo == bases[g]  # inside a group another rank owns
                 assert hi - lo <= 128
+
+
+def test_rank_tables_report_plain_ints():
+    """The per-rank figures bench.py prints (cross slots, exchange bytes, owned tokens) are plain
+    Python ints (JSON-serialisable), not numpy scalars."""
+    import json
+    from synth import workloads as W
+    from paper_2602_06072_b200 import packinfer as pk, shard
+    b = W.random_batch(31, n=24, max_len=1500, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len,
+                           pk.default_config(capacity=256, decode_chunk=256, gqa_ratio=4))
+    owner = shard.group_shard(shard.group_costs(hp), 2)
+    tb = shard.rank_tables(hp, owner, 0)
+    json.dumps({"n_cross_slots": tb["n_cross_slots"], "n_cross_rows": tb["n_cross_rows"],
+                "owned": tb["owned_tokens"], "copy_tokens": tb["copy_tokens"]})
