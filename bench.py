@@ -322,6 +322,19 @@ def e2e_steps(b, runner, steps):
 
     run(2, 20_000)                                   # warm-up (streams, pinned transfers)
     torch.cuda.synchronize()
+    # context: this host link's bandwidth for the same bytes alone (H2D of the inputs, D2H of out)
+    c0, c1, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    c0.record(s_in)
+    with torch.cuda.stream(s_in):
+        for name in host:
+            sets[1][name].copy_(host[name], non_blocking=True)
+    c1.record(s_in)
+    with torch.cuda.stream(s_in):
+        outs_h[1].copy_(outs[1], non_blocking=True)
+    c2.record(s_in)
+    torch.cuda.synchronize()
+    link = {"h2d_gbs": h2d / (c0.elapsed_time(c1) * 1e-3) / 1e9, "d2h_gbs": outs_h[1].numel() * outs_h[1].element_size()
+            / (c1.elapsed_time(c2) * 1e-3) / 1e9}
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(comp)
     s_in.wait_event(s)
@@ -331,7 +344,7 @@ def e2e_steps(b, runner, steps):
     # the last step's output landed on the host: spot-check it against the device copy
     k = (steps - 1) % 2
     assert torch.equal(outs_h[k][:4].to(outs[k].device), outs[k][:4])
-    return s.elapsed_time(e) / steps, h2d, d2h
+    return s.elapsed_time(e) / steps, h2d, d2h, link
 
 
 def decode_group_sharded(dev, rank, world, args, peaks):
@@ -1025,12 +1038,13 @@ def main():
 
     if not args.no_e2e:
         re = Runner(b, dev, h0, hc, seed=b.seed)
-        e_ms, h2d, d2h = e2e_steps(b, re, max(3, min(args.steps, 10)))
+        e_ms, h2d, d2h, link = e2e_steps(b, re, max(3, min(args.steps, 10)))
         del re
         if dist_on:
             (e_ms,) = max_over_ranks(dev, e_ms)
         result["e2e"] = {"value": units_total / (e_ms * 1e-3) / 1e12,
                          "unit": "TFLOP/s", "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                         "host_link": link,
                          "note": "pinned host buffers; H2D of step i+1 and D2H of step i-1 overlap step i "
                                  "(double-buffered device inputs/outputs, copy-in / copy-out streams)"}
 
