@@ -113,7 +113,7 @@ __device__ __forceinline__ int paged_token(const AttnParams& p, int row, int k0)
   return blk * p.page + k0 % p.page;
 }
 
-// Debug timeline: trace[(tile * 24 + event)], first TRACE_TILES tiles of CTA 0.
+// Debug timeline: trace[(tile * 32 + event)], first TRACE_TILES tiles of CTA 0.
 constexpr int TRACE_TILES = 128;
 // Compiled in only with -DPI_TRACE=1 (scripts/trace_*.py build such a variant): the hot loops of
 // the production build carry no trace checks.
@@ -122,13 +122,13 @@ constexpr int TRACE_TILES = 128;
 #endif
 __device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int ev) {
   if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
-    p.trace[tile * 24 + ev] = clock64();
+    p.trace[tile * 32 + ev] = clock64();
 }
-// Per-unit events: trace[TRACE_TILES * 24 + unit * 16 + ev], first 64 units of CTA 0 (0-3 MMA issuer, 4-6 Q
+// Per-unit events: trace[TRACE_TILES * 32 + unit * 16 + ev], first 64 units of CTA 0 (0-3 MMA issuer, 4-6 Q
 // gather, 7-11 softmax warp 4: unit start, first S landed, epilogue start (O landed), O read,
 // epilogue done).
 __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
-  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[TRACE_TILES * 24 + unit * 16 + ev] = clock64();
+  if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[TRACE_TILES * 32 + unit * 16 + ev] = clock64();
 }
 
 #ifndef PI_DEC_NSV
@@ -367,7 +367,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
             c1 = p.kv_head0 + u.kvh;
             c2 = paged_token(p, u.wk.reserved, k0);
           }
+          if (lane == 0) trace_ev(p, t, 24);
           mbar_wait(&bar[B_KFREE0 + st], ph ^ 1);
+          if (lane == 0) trace_ev(p, t, 25);
           if (elect_one()) {
             mbar_arrive_expect_tx(&bar[B_KFULL0 + st], C::TILE_BYTES);
 #pragma unroll
@@ -378,6 +380,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           __syncwarp();
           if constexpr (!F32) {
             mbar_wait(&bar[B_VFREE0 + sv], phv ^ 1);
+            if (lane == 0) trace_ev(p, t, 26);
             if (elect_one()) {
               mbar_arrive_expect_tx(&bar[B_VFULL0 + sv], C::TILE_BYTES);
 #pragma unroll
@@ -522,11 +525,13 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
         } else {
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
           issue_s(0, 0, t);
+          trace_ev(p, t, 27);
           commit(B_KFREE0 + (t % C::NSK));
           if (n > 1) {
             mbar_wait(&bar[B_KFULL0 + ((t + 1) % C::NSK)], ((t + 1) / C::NSK) & 1);
             tc_fence_after();
             issue_s(0, 1, t + 1);
+            trace_ev(p, t + 1, 27);
             commit(B_KFREE0 + ((t + 1) % C::NSK));
           }
           if (n <= 2) commit(B_QFREE);
@@ -537,10 +542,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
             mbar_wait(&bar[B_PHALF0 + b], (cnt[b] + (j >> 1)) & 1);
             trace_ev(p, tt, 1);
             mbar_wait(&bar[B_VFULL0 + (tt % C::NSV)], (tt / C::NSV) & 1);
+            trace_ev(p, tt, 28);
             if (j == 0) {
               mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
               mbar_wait(&bar[B_OFREE1], (ix[1] & 1) ^ 1);
             }
+            trace_ev(p, tt, 29);
             tc_fence_after();
             // split-K inside the CTA: keys 0..63 of every tile -> O_0 (softmax warpgroup A),
             // keys 64..127 -> O_1 (warpgroup B); the epilogue merges the two (LSE)
@@ -557,6 +564,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
               mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NSK)], ((tt + 2) / C::NSK) & 1);
               tc_fence_after();
               issue_s(0, b, tt + 2);
+              trace_ev(p, tt + 2, 27);
               commit(B_KFREE0 + ((tt + 2) % C::NSK));
               if (j + 2 == n - 1) commit(B_QFREE);
             }
@@ -1005,7 +1013,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
               if (PI_TRACE && p.trace != nullptr) spec_bits |= (spec_done ? 1u : 0u) << h;
               if (PI_TRACE && row_id == 0 && h == 1 && p.trace != nullptr && blockIdx.x == 0 &&
                   t + j < (uint32_t)TRACE_TILES)
-                p.trace[(t + j) * 24 + 17 + 2 * X] = spec_bits;
+                p.trace[(t + j) * 32 + 17 + 2 * X] = spec_bits;
               if constexpr (!F32) {
                 // pair units: P_h at 32h (over S columns already read); single units: warpgroup
                 // B's P goes over its own S columns (P1_SINGLE), never over warpgroup A's

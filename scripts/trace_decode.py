@@ -22,7 +22,7 @@ pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq //
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 TT = 128   # TRACE_TILES in attention.cu
-tr = torch.zeros(TT * 24 + 64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(TT * 32 + 64 * 16, dtype=torch.int64, device="cuda")
 L = pk.lib()
 L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
 L.packinfer_debug_trace(tr.data_ptr())
@@ -30,8 +30,8 @@ pk.packinfer_attention_decode(pb.dp, t["q"], pb.k_buf, pb.v_buf, out, None, pb.p
 torch.cuda.synchronize()
 L.packinfer_debug_trace(None)
 A = tr.cpu().numpy().astype(np.int64)
-a = A[:TT * 24].reshape(TT, 24)
-U = A[TT * 24:].reshape(64, 16)
+a = A[:TT * 32].reshape(TT, 32)
+U = A[TT * 32:].reshape(64, 16)
 u0 = U[U > 0].min()
 w = pb.plan.decode_work
 print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done  sm_start sm_gotS0 sm_epi  sm_Oread sm_epidone (n_ktiles rows)")
@@ -46,10 +46,10 @@ print("softmax A per tile (gotS -> arriveP half 1):", [int(x) for x in (a[:30, 9
 print("softmax A wait S:", [int(x) for x in (a[:30, 7] - a[:30, 6])])
 
 # per-tile softmax / MMA events (warpgroup A = key half 0 of single units), relative to "before wait S"
-names = {0: "mma_wPH", 1: "mma_gPH", 6: "smA_wS", 7: "smA_gS", 20: "smA_ldS", 22: "smA_exp", 8: "smA_P0", 9: "smA_P1",
+names = {24: "pr_wKF", 25: "pr_Kiss", 26: "pr_Viss", 27: "mma_S", 28: "mma_gV", 29: "mma_gOF", 0: "mma_wPH", 1: "mma_gPH", 6: "smA_wS", 7: "smA_gS", 20: "smA_ldS", 22: "smA_exp", 8: "smA_P0", 9: "smA_P1",
          10: "smB_wS", 11: "smB_gS", 12: "smB_P0", 13: "smB_P1", 14: "mma_PV1"}
 last = max(i for i in range(TT) if a[i, 6] > 0) if (a[:, 6] > 0).any() else -1
 print("tile " + " ".join(f"{v:>8s}" for v in names.values()))
-for i in range(max(0, last - 14), last + 1):
+for i in list(range(0, 20)) + list(range(max(20, last - 14), last + 1)):
     base = a[i, 6]
     print(f"{i:4d} " + " ".join(f"{(a[i, e] - base if a[i, e] else -1):8d}" for e in names))

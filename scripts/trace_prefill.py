@@ -19,7 +19,7 @@ pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq //
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 TT = 128   # TRACE_TILES in attention.cu
-tr = torch.zeros(TT * 24 + 64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(TT * 32 + 64 * 16, dtype=torch.int64, device="cuda")
 L = pk.lib()
 L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
 L.packinfer_debug_trace(tr.data_ptr())
@@ -27,8 +27,8 @@ pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 torch.cuda.synchronize()
 L.packinfer_debug_trace(None)
 A = tr.cpu().numpy().astype(np.int64)
-a = A[:TT * 24].reshape(TT, 24)
-U = A[TT * 24:].reshape(64, 16)
+a = A[:TT * 32].reshape(TT, 32)
+U = A[TT * 32:].reshape(64, 16)
 t0 = a[a > 0].min()
 names = ["mA_wP", "mA_gotP", "mA_S+", "mB_wP", "mB_gotP", "mB_S+",
          "sA_wS0", "sA_gS0", "sA_PH", "sA_PF", "sB_wS0", "sB_gS0", "sB_PH", "sB_PF", "mA_PV1", "mB_PV1",
