@@ -949,6 +949,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
                 }
               }
               if (!spec_done) {
+              if (row_id == 0 && X == 0) trace_ev(p, t + j, 30);
               if (!full) {
 #pragma unroll
                 for (int i = 0; i < 64; ++i) {
@@ -963,6 +964,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
               const float m_new = fmaxf(m_ref, mt * sl2);
               const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
               if (__any_sync(0xffffffffu, need)) {
+                if (row_id == 0 && X == 0) trace_ev(p, t + j, 31);
                 const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
                 if (first_half) {
                   if (j > 0) {

@@ -46,7 +46,7 @@ print("softmax A per tile (gotS -> arriveP half 1):", [int(x) for x in (a[:30, 9
 print("softmax A wait S:", [int(x) for x in (a[:30, 7] - a[:30, 6])])
 
 # per-tile softmax / MMA events (warpgroup A = key half 0 of single units), relative to "before wait S"
-names = {24: "pr_wKF", 25: "pr_Kiss", 26: "pr_Viss", 27: "mma_S", 28: "mma_gV", 29: "mma_gOF", 0: "mma_wPH", 1: "mma_gPH", 6: "smA_wS", 7: "smA_gS", 20: "smA_ldS", 22: "smA_exp", 8: "smA_P0", 9: "smA_P1",
+names = {30: "smA_exact", 31: "smA_rescl", 24: "pr_wKF", 25: "pr_Kiss", 26: "pr_Viss", 27: "mma_S", 28: "mma_gV", 29: "mma_gOF", 0: "mma_wPH", 1: "mma_gPH", 6: "smA_wS", 7: "smA_gS", 20: "smA_ldS", 22: "smA_exp", 8: "smA_P0", 9: "smA_P1",
          10: "smB_wS", 11: "smB_gS", 12: "smB_P0", 13: "smB_P1", 14: "mma_PV1"}
 last = max(i for i in range(TT) if a[i, 6] > 0) if (a[:, 6] > 0).any() else -1
 print("tile " + " ".join(f"{v:>8s}" for v in names.values()))
