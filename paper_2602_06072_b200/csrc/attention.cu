@@ -50,6 +50,9 @@
 #ifndef PI_DYN_SCHED
 #define PI_DYN_SCHED 1   // dynamic LPT list scheduling of units (0: static snake order, A/B)
 #endif
+#ifndef PI_SINGLE_S128
+#define PI_SINGLE_S128 1   // single-tile units' S: 0 two N = 64 halves, 1 one N = 128 chain,
+#endif                     // 2 N = 128 for the first two tiles only, 3 N = 128 when n_ktiles <= 4
 #ifndef PI_MERGE_ATOM
 #define PI_MERGE_ATOM 0   // merge counters: 0 atom.release, 1 atom.acq_rel, 2 one fence per unit + relaxed, 3 relaxed (A/B)
 #endif
@@ -412,19 +415,31 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       constexpr uint64_t TILE16 = C::TILE_BYTES >> 4;
       // S(X) = Q_X K(tt)^T into S/P region b, as two N = 64 halves (keys 0..63 / 64..127) so the
       // softmax can start on the first half while the second is computed.
-      auto issue_s = [&](int X, int b, uint32_t tt) {
+      auto issue_s = [&](int X, int b, uint32_t tt, bool s128) {
         const uint64_t aq = dq + X * TILE16;
         const uint64_t bk = dk + (tt % C::NSK) * TILE16;
         const uint32_t d_tmem = tmem + (b ? C::TM_S1 : C::TM_S0);
         if (elect_one()) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          if (s128) {
+            // one N = 128 chain (an N = 64 SS MMA is shared-memory-port bound: two halves cost
+            // 768 instead of 512 cycles); both halves' barriers complete with it
 #pragma unroll
             for (int kk = 0; kk < C::QK_STEPS; ++kk) {
               const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
-              mma_ss<F32>(d_tmem + h * 64, aq + off, bk + off + h * (8192 >> 4), C::IDESC_QK, kk > 0 ? 1u : 0u);
+              mma_ss<F32>(d_tmem, aq + off, bk + off, C::IDESC_QK128, kk > 0 ? 1u : 0u);
             }
-            mma_commit(&bar[B_SF00 + 2 * b + h]);
+            mma_commit(&bar[B_SF00 + 2 * b]);
+            mma_commit(&bar[B_SF00 + 2 * b + 1]);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int kk = 0; kk < C::QK_STEPS; ++kk) {
+                const uint64_t off = (uint64_t)(((kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32) >> 4);
+                mma_ss<F32>(d_tmem + h * 64, aq + off, bk + off + h * (8192 >> 4), C::IDESC_QK, kk > 0 ? 1u : 0u);
+              }
+              mma_commit(&bar[B_SF00 + 2 * b + h]);
+            }
           }
         }
         __syncwarp();
@@ -524,13 +539,15 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           ix[1] += 1;
         } else {
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
-          issue_s(0, 0, t);
+          const bool s128_pro = PI_SINGLE_S128 == 1 || PI_SINGLE_S128 == 2 || (PI_SINGLE_S128 == 3 && n <= 4);
+          const bool s128_body = PI_SINGLE_S128 == 1 || (PI_SINGLE_S128 == 3 && n <= 4);
+          issue_s(0, 0, t, s128_pro);
           trace_ev(p, t, 27);
           commit(B_KFREE0 + (t % C::NSK));
           if (n > 1) {
             mbar_wait(&bar[B_KFULL0 + ((t + 1) % C::NSK)], ((t + 1) / C::NSK) & 1);
             tc_fence_after();
-            issue_s(0, 1, t + 1);
+            issue_s(0, 1, t + 1, s128_pro);
             trace_ev(p, t + 1, 27);
             commit(B_KFREE0 + ((t + 1) % C::NSK));
           }
@@ -563,7 +580,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
             if (j + 2 < n) {
               mbar_wait(&bar[B_KFULL0 + ((tt + 2) % C::NSK)], ((tt + 2) / C::NSK) & 1);
               tc_fence_after();
-              issue_s(0, b, tt + 2);
+              issue_s(0, b, tt + 2, s128_body);
               trace_ev(p, tt + 2, 27);
               commit(B_KFREE0 + ((tt + 2) % C::NSK));
               if (j + 2 == n - 1) commit(B_QFREE);
