@@ -53,6 +53,9 @@
 #ifndef PI_SINGLE_S128
 #define PI_SINGLE_S128 1   // single-tile units' S: 0 two N = 64 halves, 1 one N = 128 chain,
 #endif                     // 2 N = 128 for the first two tiles only, 3 N = 128 when n_ktiles <= 4
+#ifndef PI_SYNCCHECK_PVH
+#define PI_SYNCCHECK_PVH 0   // 1: wait every PVH phase (synccheck-clean variant, 1-2 % slower)
+#endif
 #ifndef PI_MERGE_ATOM
 #define PI_MERGE_ATOM 0   // merge counters: 0 atom.release, 1 atom.acq_rel, 2 one fence per unit + relaxed, 3 relaxed (A/B)
 #endif
@@ -935,6 +938,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
             if (h < h_lo || h >= h_hi) continue;
             // the first half this warpgroup handles in this tile (single units: its only one)
             const bool first_half = !u.has_b || h == 0;
+            // sanitizer build: wait every PVH phase (the production build waits it only before a
+            // rare mid-tile rescale, which compute-sanitizer synccheck reports as a missing wait)
+            if (PI_SYNCCHECK_PVH && u.has_b && h == 1) {
+              mbar_wait(&bar[B_PVH0 + X], (pvh + j) & 1);
+              tc_fence_after();
+            }
             if (warp_any) {
               // Speculative half (unmasked tiles once the running max is set): exponentiate against
               // m_ref without computing the half's max.  Every P <= 2^8 (the lazy-max invariant)
@@ -996,7 +1005,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
                   }
                 } else {
                   // the first half's P.V (issued with the old max) must have landed in O
-                  mbar_wait(&bar[B_PVH0 + X], (pvh + j) & 1);
+                  if (!PI_SYNCCHECK_PVH) mbar_wait(&bar[B_PVH0 + X], (pvh + j) & 1);
                   tc_fence_after();
                   rescale_o(alpha);
 #pragma unroll

@@ -38,5 +38,30 @@ owner = shard.group_shard(shard.group_costs(pb.plan), 2)
 for rank in range(2):
     rp = shard.RankPlan(pb, owner, rank)
     pk.packinfer_relayout_kv(rp.dp, td["k_paged"], td["v_paged"], td["block_table"], pb.k_buf, pb.v_buf, 0, bd.hkv)
+# ... its decode attention + merge with the rank's renumbered slot tables (cross range neutral)
+for rank in range(2):
+    rp = shard.RankPlan(pb, owner, rank)
+    shard.neutral_cross_slots(pb.partial_o, pb.partial_lse, rp.n_cross_slots)
+    o = torch.zeros((bd.total_q, bd.hq, bd.d), dtype=torch.bfloat16, device="cuda")
+    pk.packinfer_attention_decode(rp.dp, td["q"], pb.k_buf, pb.v_buf, o, None, pb.partial_o, pb.partial_lse, r)
+    pk.packinfer_merge(rp.dp, pb.partial_o, pb.partial_lse, o, None)
+# one launch with the in-kernel LSE merge (merge warp, counters) vs the oracle
+bm = W.random_batch(402, n=10, max_len=1200, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=0.6)
+tm = W.make_tensors(bm, device="cuda")
+pbm = pk.PackedBatch(bm.kv_len, bm.q_len, bm.prefix_id, bm.prefix_len, bm.hkv, 4, bm.d, torch.bfloat16, "cuda",
+                     capacity=512, decode_chunk=128)
+om = torch.full((bm.total_q, bm.hq, bm.d), float("nan"), dtype=torch.float32, device="cuda")
+lm = torch.full((bm.hq, bm.total_q), float("nan"), dtype=torch.float32, device="cuda")
+pbm.run(tm["q"], tm["k_paged"], tm["v_paged"], tm["block_table"], om, lm, kernel_merge=True)
+H.compare(om, lm, *H.oracle_full(bm, tm))
+# paged-KV decode (NEXT-4 ablation)
+pbp = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, bd.hkv, r, bd.d, torch.bfloat16, "cuda",
+                     decode_chunk=256, flags=pk.PI_PLAN_PAGED)
+op = torch.full((bd.total_q, bd.hq, bd.d), float("nan"), dtype=torch.float32, device="cuda")
+lp = torch.full((bd.hq, bd.total_q), float("nan"), dtype=torch.float32, device="cuda")
+pk.packinfer_attention_decode_paged(pbp.dp, td["q"], td["k_paged"], td["v_paged"], td["block_table"], op, lp,
+                                    pbp.partial_o, pbp.partial_lse, r)
+pk.packinfer_merge(pbp.dp, pbp.partial_o, pbp.partial_lse, op, lp)
+H.compare(op, lp, *H.oracle_full(bd, td))
 torch.cuda.synchronize()
 print("ok")

@@ -3,7 +3,7 @@
 # relayout, fused + split attention (prefill pair units, decode single units, splits + merge),
 # fp32 toy path (kind::tf32 + V^T staging), decode group sharding.  Run under gpurun, 1 GPU.
 set -u
-OUT=gpurun_out/sanitizer
+OUT=gpurun_out/sanitizer_${1:-r02}
 mkdir -p $OUT
 PY="python scripts/dbg_sanitize.py"
 for tool in memcheck racecheck synccheck; do
