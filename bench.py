@@ -169,7 +169,7 @@ def arm_config(b, shard, world):
 class Runner:
     """Owns the device state of one batch and runs steps on one stream (double-buffered plans)."""
 
-    def __init__(self, b, device, hkv_begin, hkv_count, capacity=8192, headroom=0, seed=0):
+    def __init__(self, b, device, hkv_begin, hkv_count, capacity=8192, headroom=0, seed=0, pipeline=False):
         import torch
         from synth import workloads as W
         from paper_2602_06072_b200 import packinfer as pk
@@ -179,17 +179,28 @@ class Runner:
         self.t = W.make_tensors(b, device=device, seed=seed)
         dt = self.t["q"].dtype
         flags = int(os.environ.get("PI_BENCH_PLAN_FLAGS", "0"))      # A/B hook (ablations)
+        if hkv_count * b.hq // b.hkv <= 8:
+            # few units per SM (KV-head sharding at N >= 4): balance over L2 locality
+            flags |= pk.PI_PLAN_LPT_EXACT
         chunk = int(os.environ.get("PI_BENCH_DECODE_CHUNK", "1024"))  # A/B hook
         self.pbs = [pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, hkv_count, self.r, b.d, dt,
                                    device, capacity=capacity, headroom=headroom, flags=flags, decode_chunk=chunk)
                     for _ in range(2)]
-        self.events = [torch.cuda.Event() for _ in range(2)]
-        for e in self.events:
+        # Two streams, software-pipelined across steps: step i's host plan + upload (+ row
+        # expansion) + relayout run on `aux` into plan slot i % 2 while step i-1's attention runs on
+        # the main stream; attention i waits for its slot (ready[]), aux waits until attention i-2
+        # released the slot (done[]).  Every step still does all of its work.
+        # (pipeline=False: one stream, steps strictly sequential - for sections whose kernel
+        # roofline must not share the GPU with the next step's relayout)
+        self.stream = torch.cuda.current_stream()
+        self.aux = torch.cuda.Stream() if pipeline else self.stream
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        for e in self.done:
             e.record()
         self.q = self.t["q"][:, hkv_begin * self.r:(hkv_begin + hkv_count) * self.r]
         self.out = torch.empty((b.total_q, hkv_count * self.r, b.d), dtype=dt, device=device)
         self.lse = torch.empty((hkv_count * self.r, b.total_q), dtype=torch.float32, device=device)
-        self.stream = torch.cuda.current_stream()
         c = self.pbs[0].plan.c
         self.relayout = True
         # relayout + row expansion (inside the plan upload) + one attention launch + merge
@@ -197,27 +208,36 @@ class Runner:
         self.kernel_events = []
         self.step_events = []
 
-    def step(self, i, time_kernel=False, t=None, out=None):
+    def begin(self, ev):
+        """The aux stream's next work may not start before event `ev` (a timed region's start)."""
+        self.aux.wait_event(ev)
+
+    def step(self, i, time_kernel=False, t=None, out=None, wait_event=None):
         """One batch step on this runner's stream: host plan + upload (+ device row expansion),
         relayout (unless self.relayout is False: KV resident in the group layout), then ONE
         attention launch over every work item (packinfer_attention) and the LSE merge of split rows
         (packinfer_merge; or in-kernel with packinfer_attention_merge, see SEPARATE_MERGE).
         t / out select another (e.g. double-buffered) input set / output buffer of the same
-        shapes."""
+        shapes; wait_event: an event the step's inputs depend on (e2e: their H2D landed)."""
         pk, torch = self.pk, self.torch
         t = self.t if t is None else t
         q = self.q if t is self.t else t["q"][:, self.hkv_begin * self.r:(self.hkv_begin + self.hkv_count) * self.r]
         out = self.out if out is None else out
-        pb = self.pbs[i % 2]
+        k = i % 2
+        pb = self.pbs[k]
+        aux = self.aux
+        aux.wait_event(self.done[k])                 # attention i-2 no longer reads slot k
+        if wait_event is not None:
+            aux.wait_event(wait_event)
         if time_kernel:
             es = torch.cuda.Event(enable_timing=True)
-            es.record(self.stream)
-        self.events[i % 2].synchronize()            # host arena of this slot no longer read by H2D
-        pb.replan(self.stream)                       # host planner + async upload
-        self.events[i % 2].record(self.stream)
+            es.record(aux)
+        pb.replan(aux)                               # host planner + async upload + row expansion
         if self.relayout:
             pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf,
-                                     pb.v_buf, self.hkv_begin, self.hkv_count, self.stream)
+                                     pb.v_buf, self.hkv_begin, self.hkv_count, aux)
+        self.ready[k].record(aux)
+        self.stream.wait_event(self.ready[k])
         if time_kernel:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
@@ -228,6 +248,7 @@ class Runner:
         else:
             pk.packinfer_attention_merge(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
                                          pb.merge_counters, self.r, 0.0, self.stream)
+        self.done[k].record(self.stream)
         if time_kernel:
             e1.record(self.stream)
             self.kernel_events.append((e0, e1))
@@ -264,6 +285,7 @@ def timed_steps(runner, steps, warmup, dist_on, window=None):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
     s.record()
+    runner.begin(s)
     for i in range(steps):
         runner.step(warmup + i, time_kernel=True)
     e.record()
@@ -311,7 +333,7 @@ def e2e_steps(b, runner, steps):
             in_ready[k].record(s_in)
             comp.wait_event(in_ready[k])
             comp.wait_event(out_free[k])             # D2H of step i-2 no longer reads out[k]
-            runner.step(base + i, t=sets[k], out=outs[k])
+            runner.step(base + i, t=sets[k], out=outs[k], wait_event=in_ready[k])
             done[k].record(comp)
             s_out.wait_event(done[k])
             with torch.cuda.stream(s_out):
@@ -338,6 +360,7 @@ def e2e_steps(b, runner, steps):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(comp)
     s_in.wait_event(s)
+    runner.begin(s)
     run(steps, 10_000)
     e.record(comp)
     torch.cuda.synchronize()
@@ -926,7 +949,7 @@ def main():
         h0, hc = shard.kv_head_shard(b.hkv, rank, world)
     else:
         h0, hc = 0, b.hkv
-    runner = Runner(b, dev, h0, hc, seed=b.seed)
+    runner = Runner(b, dev, h0, hc, seed=b.seed, pipeline=True)
     flops, _, _ = algorithmic(b, runner.pbs[0].plan.c, hc)
 
     win = []
@@ -973,14 +996,22 @@ def main():
                        "row_segments": int(pc.n_segs), "rows": int(pc.n_rows),
                        "step": "plan+upload(+row expansion)+relayout+prefill(+decode+merge)",
                        "algorithmic_tflop_per_rank": flops / 1e12},
-              "roofline": roofline, "clocks": clocks, "step_latency": runner.step_latency(),
+              "roofline": roofline, "clocks": clocks,
+              "step_latency": dict(runner.step_latency(), note="pipelined steps: from the step's first op "
+                                   "(plan upload on the aux stream) to its last, incl. waiting for the previous "
+                                   "step's attention"),
               "gpu_launches": runner.launches_per_step * args.steps}
     del runner
+    # the same step strictly sequential on one stream: its isolated latency
+    rs = Runner(b, dev, h0, hc, seed=b.seed)
+    timed_steps(rs, 10, 2, dist_on)
+    result["step_latency_sequential"] = rs.step_latency()
+    del rs
 
     if dist_on and heads:
         # Strong scaling T(1) / (N T(N)) on the same batch, measured in this run: every rank also
         # times the UNSHARDED step (all KV heads) on its own GPU; T(1) = the max over ranks.
-        r1 = Runner(b, dev, 0, b.hkv, seed=b.seed)
+        r1 = Runner(b, dev, 0, b.hkv, seed=b.seed, pipeline=True)
         t1 = timed_steps(r1, args.steps, args.warmup, dist_on) / args.steps
         (t1,) = max_over_ranks(dev, t1)
         del r1
@@ -1037,7 +1068,7 @@ def main():
     result["plan"]["host_us"] = planner_us()
 
     if not args.no_e2e:
-        re = Runner(b, dev, h0, hc, seed=b.seed)
+        re = Runner(b, dev, h0, hc, seed=b.seed, pipeline=True)
         e_ms, h2d, d2h, link = e2e_steps(b, re, max(3, min(args.steps, 10)))
         del re
         if dist_on:

@@ -110,6 +110,11 @@ typedef struct {
  * packinfer_attention_decode_paged - no consolidation and no prefix co-location.  Groups, offsets
  * and the copy plan are still computed (unused).  q_len must be 1 for every request.           */
 #define PI_PLAN_PAGED 4
+/* Scheduling hint: order prefill work items by exact cost (LPT) instead of 32-key-tile cost buckets
+ * that keep emission order (L2 locality).  For launches with few units per SM - e.g. one or two KV
+ * heads per rank under KV-head sharding - balance matters more than locality (configs[1] at one
+ * KV head: kernel 0.267 -> 0.24 ms; at 8 KV heads it is ~3 % slower).                      */
+#define PI_PLAN_LPT_EXACT 8
 
 /* Fill *cfg with the defaults: C=8192, G auto, no M_max, delta=0, 128/128 tiles,
  * decode_chunk=1024, gqa_ratio=1. */

@@ -77,7 +77,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
   if (TQ != 128 || TK != 128) return fail(PI_EINVAL, "tile_q and tile_k must be 128");
   if (chunk < TK || chunk % TK) return fail(PI_EINVAL, "decode_chunk must be a positive multiple of tile_k");
   if (r < 1 || r > 16) return fail(PI_EINVAL, "gqa_ratio must be in [1, 16]");
-  if (cfg->flags & ~(PI_PLAN_NO_QPACK | PI_PLAN_DPACK | PI_PLAN_PAGED))
+  if (cfg->flags & ~(PI_PLAN_NO_QPACK | PI_PLAN_DPACK | PI_PLAN_PAGED | PI_PLAN_LPT_EXACT))
     return fail(PI_EINVAL, "unknown pi_config.flags bits");
   int64_t total_q = 0;
   for (int32_t i = 0; i < n; ++i) {
@@ -537,7 +537,7 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
       return (a.n_ktiles >> shift) > (b.n_ktiles >> shift);
     });
   };
-  lpt(pwork, PI_LPT_BUCKET_SHIFT);
+  lpt(pwork, (cfg->flags & PI_PLAN_LPT_EXACT) ? 0 : PI_LPT_BUCKET_SHIFT);
   lpt(dwork, 0);
 
   // ---------------- decode loop: next append slot per request, group drift (Eq. 4) ----------

@@ -51,6 +51,7 @@ class pi_config(C.Structure):
 PI_PLAN_NO_QPACK = 1   # ablation: one Q tile set per request (include/packinfer.h)
 PI_PLAN_DPACK = 2      # option: pack short decode suffixes of a group into one decode item
 PI_PLAN_PAGED = 4      # ablation (NEXT-4): decode items over logical tokens, read from the paged cache
+PI_PLAN_LPT_EXACT = 8  # scheduling hint: exact LPT order of prefill items (few units per SM)
 
 
 PIECE_DT = np.dtype([("request", "<i4"), ("piece", "<i4"), ("kv_begin", "<i4"), ("kv_len", "<i4"), ("group", "<i4")])
