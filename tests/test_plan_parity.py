@@ -208,3 +208,62 @@ def test_prefix_two_group_trace_bit_exact():
     hp, op = _both([180, 170, 160, 120, 190], [1] * 5, [0, -1, 0, 0, 0], [100], 300)
     assert_bit_exact(hp, op)
     assert [int(g["load"]) for g in hp.groups] == [210, 240, 170]
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("flags", [1, 2, 8, 2 | 8])
+def test_plan_options_keep_layout_and_coverage(seed, flags):
+    """PI_PLAN_NO_QPACK (1), PI_PLAN_DPACK (2) and PI_PLAN_LPT_EXACT (8) change only the execution
+    domain: Parts 1-2 stay bit-exact with the oracle and every visible (request, query, key) pair is
+    still computed exactly once (packed decode items: per-row intervals inside the hull)."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(3, 14))
+    kv = rng.integers(2, 400, size=n).astype(np.int32)
+    q = np.where(rng.random(n) < 0.6, 1, np.maximum(1, (kv * rng.random(n)).astype(np.int32))).astype(np.int32)
+    pid = np.full(n, -1, np.int32)
+    plen = []
+    if seed % 2:
+        plen = [1, 1]
+        for i in range(n):
+            if kv[i] - q[i] >= 2 and rng.random() < 0.5:
+                pid[i] = int(rng.integers(0, 2))
+                plen[pid[i]] = max(plen[pid[i]], 1)
+        for p in range(2):
+            mem = [i for i in range(n) if pid[i] == p]
+            plen[p] = int(min(kv[i] - q[i] for i in mem)) if mem else 1
+    C, r, chunk = int(rng.choice([128, 256, 1024])), int(rng.choice([1, 4])), 128
+    cfg = pk.default_config(capacity=C, headroom=2, gqa_ratio=r, decode_chunk=chunk, flags=flags)
+    hp = pk.packinfer_plan(kv, q, pid, plen, cfg)
+    op = OP.plan(list(map(int, kv)), list(map(int, q)), list(map(int, pid)), plen, C, headroom=2)
+    assert_bit_exact(hp, op)
+    check_coverage(hp, op, kv, q, pid, plen, r)
+    check_merge_map(hp, q, r)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_paged_plan_covers_logical_tokens(seed):
+    """PI_PLAN_PAGED (NEXT-4 ablation): decode items over each request's logical tokens; every
+    (request, GQA sub-head, key) is covered exactly once, chunk boundaries are tile multiples, and the
+    block-table row rides in the item's reserved field."""
+    rng = np.random.default_rng(950 + seed)
+    n = int(rng.integers(2, 12))
+    kv = rng.integers(1, 3000, size=n).astype(np.int32)
+    q = np.ones(n, np.int32)
+    r = 4
+    cfg = pk.default_config(capacity=1024, gqa_ratio=r, decode_chunk=512, flags=pk.PI_PLAN_PAGED)
+    hp = pk.packinfer_plan(kv, q, None, [], cfg)
+    rows, spans = hp.rows, hp.spans
+    seen = collections.Counter()
+    for w in hp.decode_work:
+        i = int(w["reserved"])
+        sp = spans[w["span_begin"]]
+        assert int(sp["begin"]) % 128 == 0
+        for rr in rows[w["row_begin"]:w["row_begin"] + w["row_count"]]:
+            assert int(rr["q_token"]) == i
+            for k in range(max(int(sp["begin"]), int(rr["lo"])), min(int(sp["begin"]) + int(sp["len"]), int(rr["hi"]))):
+                seen[(i, int(rr["out"]) & 15, k)] += 1
+    want = collections.Counter({(i, h, k): 1 for i in range(n) for h in range(r) for k in range(int(kv[i]))})
+    assert seen == want
+    check_merge_map(hp, q, r)
+    with pytest.raises(pk.PackInferError):
+        pk.packinfer_plan(kv, np.minimum(kv, 2), None, [], cfg)   # prefill rows are rejected
