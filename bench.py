@@ -154,6 +154,7 @@ METRIC = "packed prefill TFLOP/s (cfg2 batch step)"
 # the step's attention: one launch + the packinfer_merge launch (default, measured fastest:
 # profiles/r02b/ab_merge.txt), or PI_BENCH_SEPARATE_MERGE=0 for packinfer_attention_merge (merge in-kernel)
 SEPARATE_MERGE = os.environ.get("PI_BENCH_SEPARATE_MERGE", "1") == "1"
+PIPELINE = os.environ.get("PI_BENCH_PIPELINE", "1") == "1"       # A/B hook: headline steps pipelined
 
 
 def arm_config(b, shard, world):
@@ -949,7 +950,7 @@ def main():
         h0, hc = shard.kv_head_shard(b.hkv, rank, world)
     else:
         h0, hc = 0, b.hkv
-    runner = Runner(b, dev, h0, hc, seed=b.seed, pipeline=True)
+    runner = Runner(b, dev, h0, hc, seed=b.seed, pipeline=PIPELINE)
     flops, _, _ = algorithmic(b, runner.pbs[0].plan.c, hc)
 
     win = []

@@ -10,9 +10,11 @@ B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-mixed --no-loop -
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $OUT/launches.csv $B > $OUT/launches_bench.log 2>&1
 # prefill: the 2nd attention launch of the headline (timed step); decode: the 2nd of the cfg3 section
+# (attention launches before it: headline warm-up + step = 2, sequential-latency runner 2 + 10 = 12,
+# cfg3 warm-up 1 -> skip 15)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 1 -c 1 \
   -o $OUT/prefill $B --no-decode > $OUT/prefill.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 15 -c 1 \
   -o $OUT/decode $B > $OUT/decode.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:relayout -s 1 -c 1 \
   -o $OUT/relayout $B --no-decode > $OUT/relayout.log 2>&1
