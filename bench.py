@@ -859,6 +859,105 @@ def paged_decode(bd, rd, dev, h0, hc, steps, warmup, dist_on):
                     "(attention + merge kernel time; step = plan + upload + attention + merge)"}
 
 
+def library_context(dev, peaks, packinfer_prefill_ms, packinfer_decode_ms, steps=20):
+    """Context, not the product: library attention kernels on the same configs[1] prefill batch and
+    configs[2] decode batch on this B200 ("a real GPU baseline").  FlashAttention-2
+    varlen (flash_attn 2.8) and FlashInfer's ragged prefill read the batch's K/V as one contiguous
+    varlen tensor (gathered from the paged cache outside the timing, like our consolidation);
+    FlashInfer's paged decode reads the paged cache directly (page 128).  Same algorithmic work
+    numerators as ours; kernel time with CUDA events around the library call."""
+    import torch
+    from synth import workloads as W
+    res = {"note": "library kernels (not this repo's code) timed on the same batches; context only"}
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, e = ev(), ev()
+        a.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(e) / steps
+
+    b = make_workload("cfg2", 0)
+    t = W.make_tensors(b, device=dev, seed=b.seed)
+    flops, _, _ = algorithmic(b, None, b.hkv)
+    P = b.page_size
+    # contiguous varlen K/V [total_kv, Hkv, d] in request order (from the paged cache)
+    idx = []
+    bt = t["block_table"].cpu().numpy()
+    for i in range(b.n):
+        L = int(b.kv_len[i])
+        j = np.arange(L)
+        idx.append(bt[i, j // P] * P + j % P)
+    idx = torch.from_numpy(np.concatenate(idx).astype(np.int64)).to(dev)
+    kc = t["k_paged"].reshape(-1, b.hkv, b.d)[idx].contiguous()
+    vc = t["v_paged"].reshape(-1, b.hkv, b.d)[idx].contiguous()
+    cu = torch.from_numpy(np.concatenate([[0], np.cumsum(b.kv_len)]).astype(np.int32)).to(dev)
+    mx = int(b.kv_len.max())
+    q = t["q"]
+    ours = {"kernel_ms": packinfer_prefill_ms, "tflops": flops / (packinfer_prefill_ms * 1e-3) / 1e12}
+    res["prefill"] = {"workload": b.name + " (BASELINE.json configs[1])", "packinfer": ours}
+    try:
+        from flash_attn import flash_attn_varlen_func
+        o_fa = flash_attn_varlen_func(q, kc, vc, cu, cu, mx, mx, causal=True)
+        ms = timeit(lambda: flash_attn_varlen_func(q, kc, vc, cu, cu, mx, mx, causal=True))
+        res["prefill"]["flash_attn_2_varlen"] = {"kernel_ms": ms, "tflops": flops / (ms * 1e-3) / 1e12}
+    except Exception as e:   # context only: report, never fail the bench
+        res["prefill"]["flash_attn_2_varlen"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+        o_fa = None
+    for backend in ("auto", "cutlass"):   # FlashInfer's default and its Blackwell (CUTLASS FMHA) backend
+        key = f"flashinfer_ragged_{backend}"
+        try:
+            import flashinfer
+            ws = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+            w = flashinfer.BatchPrefillWithRaggedKVCacheWrapper(ws, "NHD", backend=backend)
+            w.plan(cu, cu, b.hq, b.hkv, b.d, causal=True, q_data_type=torch.bfloat16)
+            o_fi = w.run(q, kc, vc)
+            ms = timeit(lambda: w.run(q, kc, vc))
+            res["prefill"][key] = {"kernel_ms": ms, "tflops": flops / (ms * 1e-3) / 1e12,
+                                   "version": flashinfer.__version__}
+            if o_fa is not None:
+                res["prefill"][key]["max_abs_vs_flash_attn"] = float((o_fi.float() - o_fa.float()).abs().max())
+        except Exception as e:
+            res["prefill"][key] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+    del kc, vc, t
+    # decode: FlashInfer paged decode straight from the paged cache (no co-location, no relayout)
+    bd = make_workload("cfg3", 0)
+    td = W.make_tensors(bd, device=dev, seed=bd.seed)
+    kvb = 2 * int(bd.kv_len.sum()) * bd.hkv * bd.d * 2 + 2 * bd.n * bd.hq * bd.d * 2
+    res["decode"] = {"workload": bd.name + " (BASELINE.json configs[2])",
+                     "packinfer": {"kernel_ms": packinfer_decode_ms,
+                                   "gbs": kvb / (packinfer_decode_ms * 1e-3) / 1e9 if packinfer_decode_ms else None}}
+    try:
+        import flashinfer
+        btd = td["block_table"].cpu().numpy()
+        nblk = [-(-int(L) // P) for L in bd.kv_len]
+        indptr = torch.from_numpy(np.concatenate([[0], np.cumsum(nblk)]).astype(np.int32)).to(dev)
+        indices = torch.from_numpy(np.concatenate([btd[i, :nblk[i]] for i in range(bd.n)]).astype(np.int32)).to(dev)
+        last = torch.from_numpy(np.array([int(L) - (nb - 1) * P for L, nb in zip(bd.kv_len, nblk)], np.int32)).to(dev)
+        qd = td["q"]
+        for tc in (False, True):   # CUDA-core decode kernel / tensor-core (prefill-style) decode kernel
+            key = "flashinfer_paged_decode" + ("_tensor_cores" if tc else "")
+            try:
+                ws = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+                w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(ws, "NHD", use_tensor_cores=tc)
+                w.plan(indptr, indices, last, bd.hq, bd.hkv, bd.d, P, q_data_type=torch.bfloat16)
+                w.run(qd, (td["k_paged"], td["v_paged"]))
+                ms = timeit(lambda: w.run(qd, (td["k_paged"], td["v_paged"])))
+                res["decode"][key] = {"kernel_ms": ms, "gbs": kvb / (ms * 1e-3) / 1e9}
+            except Exception as e:
+                res["decode"][key] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+    except Exception as e:
+        res["decode"]["flashinfer_paged_decode"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+    del td
+    return res
+
+
 def section_prefill(name, dev, h0, hc, args, peaks, dist_on, sampler, seed_rank):
     """A prefill step of one BASELINE batch on this rank's KV heads (TFLOP/s over the prefill
     kernel time and over the step)."""
@@ -897,6 +996,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-mixed", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-context", action="store_true", help="skip the library-kernel context section")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args, "cfg2")
@@ -1067,6 +1167,10 @@ def main():
         result["mixed"] = mixed_section(dev, h0, hc, rank, args, peaks, dist_on)
 
     result["plan"]["host_us"] = planner_us()
+
+    if not args.no_context and rank == 0 and world == 1:
+        result["library_context"] = library_context(dev, peaks, pre_ms,
+                                                     result.get("decode", {}).get("kernel_ms"))
 
     if not args.no_e2e:
         re = Runner(b, dev, h0, hc, seed=b.seed, pipeline=True)
