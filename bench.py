@@ -859,7 +859,7 @@ def paged_decode(bd, rd, dev, h0, hc, steps, warmup, dist_on):
                     "(attention + merge kernel time; step = plan + upload + attention + merge)"}
 
 
-def library_context(dev, peaks, packinfer_prefill_ms, packinfer_decode_ms, steps=20):
+def library_context(dev, peaks, packinfer_prefill_ms, packinfer_decode_ms, packinfer_decode4_ms=None, steps=20):
     """Context, not the product: library attention kernels on the same configs[1] prefill batch and
     configs[2] decode batch on this B200 ("a real GPU baseline").  FlashAttention-2
     varlen (flash_attn 2.8) and FlashInfer's ragged prefill read the batch's K/V as one contiguous
@@ -927,12 +927,23 @@ def library_context(dev, peaks, packinfer_prefill_ms, packinfer_decode_ms, steps
             res["prefill"][key] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
     del kc, vc, t
     # decode: FlashInfer paged decode straight from the paged cache (no co-location, no relayout)
-    bd = make_workload("cfg3", 0)
+    for sec, name, ours_ms in (("decode", "cfg3", packinfer_decode_ms), ("decode_shared_prefix", "cfg4_decode",
+                                                                         packinfer_decode4_ms)):
+        res[sec] = library_decode(dev, name, ours_ms, timeit)
+    return res
+
+
+def library_decode(dev, name, ours_ms, timeit):
+    """FlashInfer paged decode (CUDA-core and tensor-core kernels) on one BASELINE decode batch;
+    bytes = the KV each request reads through its block table (shared prefixes once per request)."""
+    import torch
+    from synth import workloads as W
+    bd = make_workload(name, 0)
     td = W.make_tensors(bd, device=dev, seed=bd.seed)
+    P = bd.page_size
     kvb = 2 * int(bd.kv_len.sum()) * bd.hkv * bd.d * 2 + 2 * bd.n * bd.hq * bd.d * 2
-    res["decode"] = {"workload": bd.name + " (BASELINE.json configs[2])",
-                     "packinfer": {"kernel_ms": packinfer_decode_ms,
-                                   "gbs": kvb / (packinfer_decode_ms * 1e-3) / 1e9 if packinfer_decode_ms else None}}
+    res = {"workload": bd.name, "flashinfer_kv_bytes": kvb,
+           "packinfer": {"kernel_ms": ours_ms, "note": "packed layout: Eq. 5 bytes (prefix once per group)"}}
     try:
         import flashinfer
         btd = td["block_table"].cpu().numpy()
@@ -949,11 +960,11 @@ def library_context(dev, peaks, packinfer_prefill_ms, packinfer_decode_ms, steps
                 w.plan(indptr, indices, last, bd.hq, bd.hkv, bd.d, P, q_data_type=torch.bfloat16)
                 w.run(qd, (td["k_paged"], td["v_paged"]))
                 ms = timeit(lambda: w.run(qd, (td["k_paged"], td["v_paged"])))
-                res["decode"][key] = {"kernel_ms": ms, "gbs": kvb / (ms * 1e-3) / 1e9}
+                res[key] = {"kernel_ms": ms, "gbs": kvb / (ms * 1e-3) / 1e9}
             except Exception as e:
-                res["decode"][key] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+                res[key] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
     except Exception as e:
-        res["decode"]["flashinfer_paged_decode"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+        res["flashinfer_paged_decode"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
     del td
     return res
 
@@ -1169,8 +1180,9 @@ def main():
     result["plan"]["host_us"] = planner_us()
 
     if not args.no_context and rank == 0 and world == 1:
-        result["library_context"] = library_context(dev, peaks, pre_ms,
-                                                     result.get("decode", {}).get("kernel_ms"))
+        result["library_context"] = library_context(
+            dev, peaks, pre_ms, result.get("decode", {}).get("kernel_ms"),
+            result.get("shared_prefix", {}).get("decode", {}).get("kernel_ms"))
 
     if not args.no_e2e:
         re = Runner(b, dev, h0, hc, seed=b.seed, pipeline=True)
