@@ -407,8 +407,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
     // tcgen05.mma / commit is issued by one elected lane (no per-MMA waterfall loops).
     {
       uint32_t t = 0, item = 0;
-      uint32_t cnt[2] = {0, 0};   // completions so far of SFULL/PFULL of region 0 / 1
-      uint32_t ix[2] = {0, 0};    // completions so far of OFULL/OFREE of slot 0 / 1
+      // completions so far of SFULL/PFULL of region 0 / 1 and of OFULL/OFREE (both slots alike).
+      // Scalars, not arrays: a runtime region index would put an array in local memory
+      uint32_t cntA = 0, cntB = 0, ix = 0;
+      auto cnt = [&](int x) { return x ? cntB : cntA; };
       // Descriptors are built once; each k-step adds a compile-time offset to the 14-bit start
       // address field (all smem offsets < 256 KB, so the field never carries).
       const uint64_t dq = sdesc_sw128(sbase + C::OFF_Q, 16, 1024);
@@ -508,14 +510,14 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
             const uint32_t tt = t + j;
             for (int X = 0; X < 2; ++X) {
               trace_ev(p, tt, 0 + 3 * X);
-              mbar_wait(&bar[B_PHALF0 + X], (cnt[X] + j) & 1);
+              mbar_wait(&bar[B_PHALF0 + X], (cnt(X) + j) & 1);
               trace_ev(p, tt, 1 + 3 * X);
               if (X == 0) mbar_wait(&bar[B_VFULL0 + (tt % C::NSV)], (tt / C::NSV) & 1);
-              if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix[X] & 1) ^ 1);
+              if (j == 0) mbar_wait(&bar[B_OFREE0 + X], (ix & 1) ^ 1);
               tc_fence_after();
               issue_pv(X, X ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
               commit(B_PVH0 + X);
-              mbar_wait(&bar[B_PFULL0 + X], (cnt[X] + j) & 1);
+              mbar_wait(&bar[B_PFULL0 + X], (cnt(X) + j) & 1);
               tc_fence_after();
               issue_pv(X, (X ? C::TM_S1 : C::TM_S0) + 32, tt, false, 1);
               trace_ev(p, tt, 14 + X);
@@ -536,10 +538,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
               }
             }
           }
-          cnt[0] += n;
-          cnt[1] += n;
-          ix[0] += 1;
-          ix[1] += 1;
+          cntA += n;
+          cntB += n;
+          ix += 1;
         } else {
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
           const bool s128_pro = PI_SINGLE_S128 == 1 || PI_SINGLE_S128 == 2 || (PI_SINGLE_S128 == 3 && n <= 4);
@@ -559,20 +560,20 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
             const uint32_t tt = t + j;
             const int b = j & 1;
             trace_ev(p, tt, 0);
-            mbar_wait(&bar[B_PHALF0 + b], (cnt[b] + (j >> 1)) & 1);
+            mbar_wait(&bar[B_PHALF0 + b], (cnt(b) + (j >> 1)) & 1);
             trace_ev(p, tt, 1);
             mbar_wait(&bar[B_VFULL0 + (tt % C::NSV)], (tt / C::NSV) & 1);
             trace_ev(p, tt, 28);
             if (j == 0) {
-              mbar_wait(&bar[B_OFREE0], (ix[0] & 1) ^ 1);
-              mbar_wait(&bar[B_OFREE1], (ix[1] & 1) ^ 1);
+              mbar_wait(&bar[B_OFREE0], (ix & 1) ^ 1);
+              mbar_wait(&bar[B_OFREE1], (ix & 1) ^ 1);
             }
             trace_ev(p, tt, 29);
             tc_fence_after();
             // split-K inside the CTA: keys 0..63 of every tile -> O_0 (softmax warpgroup A),
             // keys 64..127 -> O_1 (warpgroup B); the epilogue merges the two (LSE)
             issue_pv(0, b ? C::TM_S1 : C::TM_S0, tt, j == 0, 0);
-            mbar_wait(&bar[B_PFULL0 + b], (cnt[b] + (j >> 1)) & 1);
+            mbar_wait(&bar[B_PFULL0 + b], (cnt(b) + (j >> 1)) & 1);
             tc_fence_after();
             issue_pv(1, (b ? C::TM_S1 : C::TM_S0) + C::P1_SINGLE, tt, j == 0, 1);
             commit(B_VFREE0 + (tt % C::NSV));
@@ -589,10 +590,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
               if (j + 2 == n - 1) commit(B_QFREE);
             }
           }
-          cnt[0] += (n + 1) >> 1;
-          cnt[1] += n >> 1;
-          ix[0] += 1;
-          ix[1] += 1;
+          cntA += (n + 1) >> 1;
+          cntB += n >> 1;
+          ix += 1;
         }
         trace_unit(p, item, 3);
         t += n;
@@ -787,10 +787,13 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
     const int row_id = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t o_tm = tmem + lane_base + (X ? C::TM_O1 : C::TM_O0);
-    uint32_t cnt[2] = {0, 0}, ix = 0, t = 0;
+    // completions so far of SF[b][0] / P of region b (scalars: see the MMA issuer)
+    uint32_t cntA = 0, cntB = 0, ix = 0, t = 0;
+    auto cnt = [&](int x) { return x ? cntB : cntA; };
     // completions so far of SF[b][1] (S half 1 of region b): only single-tile units compute S in
     // two halves; pair units' one N = 128 chain completes SF[X][0] alone
-    uint32_t cnt1[2] = {0, 0};
+    uint32_t cnt1A = 0, cnt1B = 0;
+    auto cnt1 = [&](int x) { return x ? cnt1B : cnt1A; };
     uint32_t pvh = 0;                       // completions so far of PVH[X] (this slot's P.V halves)
     uint32_t epi = 0;                       // units handed to the merge warp so far
     const float NEG_INF = -INFINITY;
@@ -874,9 +877,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           };
           if (row_id == 0) trace_ev(p, t + j, 6 + 4 * X);
           if (u.has_b || X == 0)
-            mbar_wait(&bar[B_SF00 + 2 * b], (cnt[b] + kb) & 1);   // pair units: the whole N = 128 S
+            mbar_wait(&bar[B_SF00 + 2 * b], (cnt(b) + kb) & 1);   // pair units: the whole N = 128 S
           else
-            mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt1[b] + kb) & 1);
+            mbar_wait(&bar[B_SF00 + 2 * b + 1], (cnt1(b) + kb) & 1);
           tc_fence_after();
           if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
           if (j == 0 && warp == C::ROLE && lane == 0) trace_unit(p, ix, 8);
@@ -1181,13 +1184,13 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
         ++epi;
       }
       if (u.has_b) {
-        cnt[0] += n;
-        cnt[1] += n;
+        cntA += n;
+        cntB += n;
       } else {
-        cnt[0] += (n + 1) >> 1;
-        cnt[1] += n >> 1;
-        cnt1[0] += (n + 1) >> 1;
-        cnt1[1] += n >> 1;
+        cntA += (n + 1) >> 1;
+        cntB += n >> 1;
+        cnt1A += (n + 1) >> 1;
+        cnt1B += n >> 1;
       }
       if (u.has_b) pvh += n;   // PVH completes for pair units only
       t += n;

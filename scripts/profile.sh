@@ -5,7 +5,7 @@ set -u
 TAG=${1:-r02}
 OUT=gpurun_out/prof_$TAG
 mkdir -p $OUT
-B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-mixed --no-loop --no-prefix"
+B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-mixed --no-loop --no-prefix --no-context"
 # launch list of one short bench (kernel durations, cold-cache + serialised: shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $OUT/launches.csv $B > $OUT/launches_bench.log 2>&1
