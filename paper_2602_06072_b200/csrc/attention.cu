@@ -137,6 +137,9 @@ __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, i
   if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[TRACE_TILES * 32 + unit * 16 + ev] = clock64();
 }
 
+#ifndef PI_DEC_SLICE
+#define PI_DEC_SLICE 1   // lane-sliced single-tile units (<= kSliceRows rows): see unit_sliced()
+#endif
 #ifndef PI_DEC_NSV
 #define PI_DEC_NSV 3   // V stages of decode-only (single-tile) launches: V is held until P.V
 #endif
@@ -163,7 +166,11 @@ struct AttnCfg {
   static constexpr int OFF_V = OFF_K + NSK * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_V + NSV * TILE_BYTES;
   static constexpr int OFF_XCH = OFF_BAR + 512;       // single units: (m, l, l_rounded) of both warpgroups
-  static constexpr int SMEM = OFF_XCH + 2 * 128 * 16 + 1024;  // + alignment slack
+  // lane-sliced single units: the four lane quarters' O partials of <= kSliceRows rows (padded rows)
+  static constexpr int OBUF_STRIDE = D + 4;
+  static constexpr int OFF_OBUF = OFF_XCH + 2 * 128 * 16;
+  static constexpr int OBUF_BYTES = ((UK & 2) && !F32) ? 4 * 8 * OBUF_STRIDE * 4 : 0;
+  static constexpr int SMEM = OFF_OBUF + OBUF_BYTES + 1024;  // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
   // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
   static constexpr uint32_t P1_SINGLE = F32 ? 64u : 96u;
@@ -244,6 +251,21 @@ __device__ __forceinline__ void ring_release(uint64_t* bar, int k, int lane) {
 // UK (unit kinds a kernel instance handles): 1 = pair units only (prefill launch, even r),
 // 2 = single-tile units only (decode launch, fp32 operands), 3 = both.  With one kind the
 // compiler drops the other kind's code from every role loop.
+// Lane-sliced single-tile units.  A decode unit of r rows (one request's GQA group: 4 for
+// Llama-3-8B) leaves 124 of 128 TMEM lanes idle, and only the two softmax warps owning lane quarter
+// 0 would work: each exponentiates 64 columns per tile while the other six wait, so short units are
+// bound by that one warp's latency (profiles/r02k/decode_cfg4_trace.md).  With <= kSliceRows rows
+// the Q gather replicates the rows into all four lane quarters (lanes 32q + i, q = 0..3), so every
+// quarter computes the same S rows, and warp (X, q) takes only keys [64X + 16q, 64X + 16q + 16) of
+// every tile: its own running max / sums and P (zero outside its 16 keys) into O_X at its lanes.
+// The eight partials of a row (2 key halves x 4 quarters) are LSE-merged in the epilogue exactly
+// as the two split-K halves are (reading R10), the quarters summed in a fixed order through smem.
+constexpr int kSliceRows = 8;
+template <int UK, bool F32>
+__device__ __forceinline__ bool unit_sliced(const Unit& u) {
+  return PI_DEC_SLICE && (UK & 2) && !F32 && !u.has_b && u.wk.row_count <= kSliceRows;
+}
+
 template <int UK>
 __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
   Unit u;
@@ -615,18 +637,23 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       mbar_wait(&bar[B_QFREE], (item & 1) ^ 1);
       trace_unit(p, item, 5);
       const int rows = u.wk.row_count;
-      const int groups = (rows + 3) >> 2;
+      // lane-sliced units: the rows again at the start of every lane quarter (row groups 8q + g)
+      const bool sl = unit_sliced<UK, F32>(u);
+      const int gpq = (rows + 3) >> 2;
+      const int groups = sl ? 4 * gpq : gpq;
       if (lane == 0) mbar_arrive_expect_tx(&bar[B_QFULL], (uint32_t)(nt * groups * C::ATOMS * 512));
       __syncwarp();
       if (lane < groups) {
+        const int gi = sl ? lane % gpq : lane;
+        const int dst_group = sl ? 8 * (lane / gpq) + gi : lane;
         int32_t ri[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const pi_row row = p.rows[u.wk.row_begin + min(4 * lane + e, rows - 1)];
+          const pi_row row = p.rows[u.wk.row_begin + min(4 * gi + e, rows - 1)];
           ri[e] = row.q_token * p.q_heads_stride + u.head0 + (row.out & 15);
         }
         for (int X = 0; X < nt; ++X) {
-          uint8_t* dst = smem + C::OFF_Q + X * C::TILE_BYTES + lane * 512;
+          uint8_t* dst = smem + C::OFF_Q + X * C::TILE_BYTES + dst_group * 512;
 #pragma unroll
           for (int a = 0; a < C::ATOMS; ++a)
             tma_gather4(dst + a * C::ATOM_BYTES, &tmQ, &bar[B_QFULL], a * C::ATOM_ELEMS, ri[0] + X, ri[1] + X,
@@ -819,7 +846,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
     pi_span nsp = {0, 0};
     auto prefetch = [&](int wn) {
       nu = get_unit<UK>(p, wn);
-      nrow = row_id < nu.wk.row_count ? p.rows[nu.wk.row_begin + row_id] : pi_row{0, 0, 0, 0};
+      const int ri = unit_sliced<UK, F32>(nu) ? lane : row_id;   // sliced: row `lane` in every quarter
+      nrow = ri < nu.wk.row_count ? p.rows[nu.wk.row_begin + ri] : pi_row{0, 0, 0, 0};
       nsp = p.spans[nu.wk.span_begin];
     };
     int w = ring_get(uring, bar, 0);
@@ -836,7 +864,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       // pair units: warpgroup X owns tile X (both key halves); single-tile units: warpgroup X owns
       // key half X of every tile (split-K inside the CTA, merged in the epilogue)
       const int h_lo = u.has_b ? 0 : X, h_hi = u.has_b ? 2 : X + 1;
-      const bool valid = row_id < wk.row_count;
+      const bool sl = unit_sliced<UK, F32>(u);
+      const bool valid = (sl ? lane : row_id) < wk.row_count;
       const bool warp_any = wq * 32 < wk.row_count;
       const pi_row row = row_pf;
       float m_ref = NEG_INF, l = 0.f, lr = 0.f;   // running max (log2 units), exact / rounded-P sums
@@ -883,6 +912,87 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           tc_fence_after();
           if (row_id == 0) trace_ev(p, t + j, 7 + 4 * X);
           if (j == 0 && warp == C::ROLE && lane == 0) trace_unit(p, ix, 8);
+          if constexpr ((UK & 2) && !F32) {
+            if (sl) {
+              // lane-sliced unit: this warp's 16 keys [cs, cs + 16) of the tile (unit_sliced())
+              const int cs = 64 * X + 16 * wq;
+              uint32_t s16[16];
+              tmem_ld16(region + cs, s16);
+              tmem_wait_ld();
+              reg_fence(s16);
+              const int lo = max(c_lo - cs, 0), hi = min(c_hi - cs, 16);
+              const bool sfull = lo == 0 && hi == 16;
+              uint32_t p8[8];
+              float e_sum = 0.f, r_sum = 0.f;   // exact / bf16-rounded sums of this slice's P
+              // P = exp2(s * scale_log2 + nm) (MUFU), packed bf16 into p8, both row sums
+              auto exp16 = [&](float nm) {
+                const uint64_t SL2 = f2(sl2, sl2), NM = f2(nm, nm);
+                uint64_t acc = f2(0.f, 0.f), racc = f2(0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const uint64_t x = f2_fma(f2(__uint_as_float(s16[2 * i]), __uint_as_float(s16[2 * i + 1])), SL2, NM);
+                  const uint64_t e = f2(ex2(f2_lo(x)), ex2(f2_hi(x)));
+                  acc = f2_add(acc, e);
+                  p8[i] = pack_bf16(f2_lo(e), f2_hi(e));
+                  uint32_t rl, rh;
+                  asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(rl) : "r"(p8[i]));
+                  asm("prmt.b32 %0, %1, 0, 0x3244;" : "=r"(rh) : "r"(p8[i]));
+                  racc = f2_add(racc, f2(__uint_as_float(rl), __uint_as_float(rh)));
+                }
+                e_sum = f2_lo(acc) + f2_hi(acc);
+                r_sum = f2_lo(racc) + f2_hi(racc);
+              };
+              bool done = false;
+              // speculative slice against the running max, certified by its sum (as above)
+              if (__all_sync(0xffffffffu, !valid || (sfull && m_ref != NEG_INF))) {
+                exp16(-m_ref);
+                done = !__any_sync(0xffffffffu, valid && !(e_sum <= 256.0f));
+              }
+              if (!done) {
+                if (!sfull) {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i)
+                    if (!(i >= lo && i < hi)) s16[i] = __float_as_uint(NEG_INF);
+                }
+                float mx = NEG_INF;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) mx = fmaxf(mx, __uint_as_float(s16[i]));
+                const float m_new = fmaxf(m_ref, mx * sl2);
+                const bool need = valid && (m_ref != NEG_INF) && (m_new > m_ref + 8.0f);
+                if (__any_sync(0xffffffffu, need)) {
+                  const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
+                  if (j > 0) {
+                    const uint32_t tp = t + j - 1;   // P.V(j-1) must have landed in O
+                    mbar_wait(&bar[B_VFREE0 + (tp % C::NSV)], (tp / C::NSV) & 1);
+                    tc_fence_after();
+                    rescale_o(alpha);
+                  }
+                  if (need) {
+                    l *= alpha;
+                    lr *= alpha;
+                    m_ref = m_new;
+                  }
+                }
+                if (m_ref == NEG_INF) m_ref = m_new;
+                exp16(m_ref != NEG_INF ? -m_ref : NEG_INF);
+              }
+              // P of this warpgroup's key half: this warp's 8 packed columns, zeros for the others
+              const uint32_t p_base = region + (X ? C::P1_SINGLE : 0u);
+              const uint32_t z8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+              tmem_st8(p_base + 8u * wq, p8);
+              tmem_st8(p_base + 8u * ((wq + 1) & 3), z8);
+              tmem_st8(p_base + 8u * ((wq + 2) & 3), z8);
+              tmem_st8(p_base + 8u * ((wq + 3) & 3), z8);
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&bar[(X == 0 ? B_PHALF0 : B_PFULL0) + b]);
+              if (valid) {
+                l += e_sum;
+                lr += r_sum;
+              }
+              continue;
+            }
+          }
           if (warp_any) {
             load_s(region + 64u * h_lo);
             tmem_wait_ld();
@@ -1088,9 +1198,101 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       // 0..63 / 64..127 of every tile with partial accumulators O_0 / O_1; merge them (reading
       // R10: M = max, w = 2^(m - M), L = sum w l) and let warpgroup X write output columns
       // [X D/2, (X+1) D/2).
-      float sc0, sc1 = 0.f, lse_v;
+      float sc0 = 0.f, sc1 = 0.f, lse_v = 0.f;
       int c4_begin = 0, c4_end = D / 32;
-      if (u.has_b) {
+      if constexpr ((UK & 2) && !F32) {
+        if (sl) {
+          // lane-sliced unit: merge the row's eight partials (key half X' x lane quarter q, reading
+          // R10), scale this quarter's O_0 / O_1 into the smem partial of quarter wq, then sum the
+          // four quarters in a fixed order (bitwise reproducible) and store.
+          float4* xch = reinterpret_cast<float4*>(smem + C::OFF_XCH);
+          xch[X * 128 + row_id] = make_float4(m_ref, l, lr, 0.f);
+          named_bar_sync(1, 256);
+          float M = NEG_INF, mq[8], lq[8], rq[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 o = xch[(k >> 2) * 128 + (k & 3) * 32 + lane];
+            mq[k] = o.x;
+            lq[k] = o.y;
+            rq[k] = o.z;
+            if (o.y > 0.f) M = fmaxf(M, o.x);
+          }
+          float L = 0.f, LR = 0.f, w0 = 0.f, w1 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float wk_ = lq[k] > 0.f ? ex2(mq[k] - M) : 0.f;
+            L += lq[k] * wk_;
+            LR += rq[k] * wk_;
+            if (k == wq) w0 = wk_;
+            if (k == 4 + wq) w1 = wk_;
+          }
+          const float inv = LR > 0.f ? 1.0f / LR : 0.f;
+          lse_v = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
+          float* ob = reinterpret_cast<float*>(smem + C::OFF_OBUF);
+#pragma unroll
+          for (int c4 = 0; c4 < D / 32; ++c4) {
+            if (c4 < X * (D / 64) || c4 >= (X + 1) * (D / 64)) continue;
+            uint32_t o0[32], o1[32];
+            tmem_ld32(tmem + lane_base + C::TM_O0 + c4 * 32, o0);
+            tmem_ld32(tmem + lane_base + C::TM_O1 + c4 * 32, o1);
+            tmem_wait_ld();
+            reg_fence(o0);
+            reg_fence(o1);
+            if (valid) {
+              float* dst = ob + (wq * kSliceRows + lane) * C::OBUF_STRIDE + c4 * 32;
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                float4 f;
+                f.x = fmaf(__uint_as_float(o0[4 * v + 0]), w0 * inv, __uint_as_float(o1[4 * v + 0]) * (w1 * inv));
+                f.y = fmaf(__uint_as_float(o0[4 * v + 1]), w0 * inv, __uint_as_float(o1[4 * v + 1]) * (w1 * inv));
+                f.z = fmaf(__uint_as_float(o0[4 * v + 2]), w0 * inv, __uint_as_float(o1[4 * v + 2]) * (w1 * inv));
+                f.w = fmaf(__uint_as_float(o0[4 * v + 3]), w0 * inv, __uint_as_float(o1[4 * v + 3]) * (w1 * inv));
+                reinterpret_cast<float4*>(dst)[v] = f;
+              }
+            }
+          }
+          named_bar_sync(1, 256);
+          {
+            constexpr int V4 = D / 4;
+            const int tid = threadIdx.x - 32 * C::ROLE;   // 0..255
+            const int rr = tid / V4, c = (tid % V4) * 4;
+            if (rr < wk.row_count) {
+              float4 a[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) a[q] = *reinterpret_cast<const float4*>(ob + (q * kSliceRows + rr) * C::OBUF_STRIDE + c);
+              float4 f;
+              f.x = (a[0].x + a[1].x) + (a[2].x + a[3].x);
+              f.y = (a[0].y + a[1].y) + (a[2].y + a[3].y);
+              f.z = (a[0].z + a[1].z) + (a[2].z + a[3].z);
+              f.w = (a[0].w + a[1].w) + (a[2].w + a[3].w);
+              const pi_row rw = p.rows[wk.row_begin + rr];
+              const int rslot = (rw.out >> 4) - 1;
+              const int rhead = u.head0 + (rw.out & 15);
+              if (rslot < 0) {
+                if (!p.out_f32) {
+                  uint8_t* dst = p.out + ((int64_t)rw.q_token * p.out_row_stride + (int64_t)rhead * D + c) * 2;
+                  *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(f.x, f.y), pack_bf16(f.z, f.w));
+                } else {
+                  uint8_t* dst = p.out + ((int64_t)rw.q_token * p.out_row_stride + (int64_t)rhead * D + c) * 4;
+                  *reinterpret_cast<float4*>(dst) = f;
+                }
+              } else {
+                *reinterpret_cast<float4*>(p.partial_o + ((int64_t)rslot * p.hq_count + rhead) * D + c) = f;
+              }
+            }
+          }
+          if (valid && X == 0 && wq == 0) {
+            if (slot < 0) {
+              if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
+            } else {
+              p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
+            }
+          }
+          c4_end = 0;   // nothing left for the generic store path below
+        }
+      }
+      if (sl) {
+      } else if (u.has_b) {
         sc0 = lr > 0.f ? 1.0f / lr : 0.f;
         lse_v = l > 0.f ? (m_ref + __log2f(l)) * 0.69314718055994530942f : NEG_INF;
       } else {
@@ -1163,7 +1365,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           }
         }
       }
-      if (valid && (u.has_b || X == 0)) {
+      if (valid && !sl && (u.has_b || X == 0)) {
         if (slot < 0) {
           if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
         } else {
