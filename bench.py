@@ -245,6 +245,9 @@ class Runner:
         if SEPARATE_MERGE:   # A/B hook: attention launch + packinfer_merge launch
             pk.packinfer_attention(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
                                    self.r, 0.0, self.stream)
+            if time_kernel:
+                em = torch.cuda.Event(enable_timing=True)
+                em.record(self.stream)
             pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, out, self.lse, self.stream)
         else:
             pk.packinfer_attention_merge(pb.dp, q, pb.k_buf, pb.v_buf, out, self.lse, pb.partial_o, pb.partial_lse,
@@ -252,7 +255,8 @@ class Runner:
         self.done[k].record(self.stream)
         if time_kernel:
             e1.record(self.stream)
-            self.kernel_events.append((e0, e1))
+            # the attention launch alone (the roofline kernel) and the whole attention + merge
+            self.kernel_events.append((e0, em if SEPARATE_MERGE else e1, e1))
             ee = torch.cuda.Event(enable_timing=True)
             ee.record(self.stream)
             self.step_events.append((es, ee))
@@ -264,8 +268,14 @@ class Runner:
         return {"median_ms": float(np.median(v)), "p90_ms": float(np.percentile(v, 90)), "n": int(v.size)}
 
     def kernel_ms(self):
-        """Average time of the step's attention launch (prefill + decode items + in-kernel merge)."""
-        v = [a.elapsed_time(b) for a, b in self.kernel_events]
+        """Average time of the step's attention launch (prefill + decode items; + the merge when it
+        runs in-kernel): the roofline kernel."""
+        v = [a.elapsed_time(b) for a, b, _ in self.kernel_events]
+        return sum(v) / len(v) if v else 0.0
+
+    def merge_ms(self):
+        """Average time of the separate LSE-merge launch after it (0 with the in-kernel merge)."""
+        v = [b.elapsed_time(c) for _, b, c in self.kernel_events]
         return sum(v) / len(v) if v else 0.0
 
 
@@ -781,9 +791,9 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
     steps = max(10, args.steps)
     win = []
     dms = timed_steps(rd, steps, args.warmup, dist_on, win) / steps
-    dec_ms = rd.kernel_ms()
+    dec_ms, mrg_ms = rd.kernel_ms(), rd.merge_ms()
     if dist_on:
-        dms, dec_ms = max_over_ranks(dev, dms, dec_ms)
+        dms, dec_ms, mrg_ms = max_over_ranks(dev, dms, dec_ms, mrg_ms)
     ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
     # KV resident in the group layout (the producer writes new tokens there, packinfer_append_kv):
     # the step is host plan + upload + ONE attention launch with the merge inside - no relayout
@@ -794,7 +804,8 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
         rms, rk = max_over_ranks(dev, rms, rk)
     c = rd.pbs[0].plan.c
     paged = paged_decode(bd, rd, dev, h0, hc, steps, args.warmup, dist_on)
-    out = {"ms_per_step": dms, "kernel_ms": dec_ms, "kv_bytes": kvb, "qo_bytes": qob, "achieved_gbs": ach,
+    out = {"ms_per_step": dms, "kernel_ms": dec_ms, "merge_ms": mrg_ms, "kv_bytes": kvb, "qo_bytes": qob,
+           "achieved_gbs": ach,
            "peak_gbs": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
            "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9, "work_items": int(c.n_decode_work),
            "partial_slots": int(c.n_partial_slots), "groups": int(c.n_groups),
@@ -804,7 +815,8 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
                         "step_gbs": (kvb + qob) / (rms * 1e-3) / 1e9,
                         "gpu_launches_per_step": rd.launches_per_step - 1,
                         "note": "KV resident in the group-contiguous layout: plan + upload (+ row expansion) "
-                                "+ one attention launch + merge; no relayout"},
+                                "+ one attention launch + merge; no relayout (kernel_ms: the attention launch; "
+                                "the previous step's attention may leave part of the KV in L2)"},
            "paged": paged}
     del rd
     return out
@@ -831,8 +843,8 @@ def paged_decode(bd, rd, dev, h0, hc, steps, warmup, dist_on):
         a.record(st)
         pk.packinfer_attention_decode_paged(pb.dp, rd.q, rd.t["k_paged"], rd.t["v_paged"], rd.t["block_table"],
                                             rd.out, rd.lse, pb.partial_o, pb.partial_lse, r, h0, hc, 0.0, st)
-        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, rd.out, rd.lse, st)
         e.record(st)
+        pk.packinfer_merge(pb.dp, pb.partial_o, pb.partial_lse, rd.out, rd.lse, st)
         if timed:
             kern.append((a, e))
 
@@ -856,7 +868,7 @@ def paged_decode(bd, rd, dev, h0, hc, steps, warmup, dist_on):
     return {"ms_per_step": ms, "kernel_ms": kms, "kv_tokens": kv_tokens, "kv_bytes": kvb,
             "achieved_gbs": (kvb + qob) / (kms * 1e-3) / 1e9, "work_items": None,
             "note": "PI_PLAN_PAGED: decode straight from the paged cache, no relayout, no prefix co-location "
-                    "(attention + merge kernel time; step = plan + upload + attention + merge)"}
+                    "(kernel_ms: the attention launch, as for the packed kernel; step = plan + upload + attention + merge)"}
 
 
 def library_context(dev, peaks, packinfer_prefill_ms, packinfer_decode_ms, packinfer_decode4_ms=None, steps=20):
@@ -1051,7 +1063,8 @@ def main():
     peaks, peak_src = load_peaks()
     dev = torch.device("cuda", local)
     sampler = ClockSampler(local)
-    sampler.start()
+    if os.environ.get("PI_BENCH_NO_CLOCKS") != "1":   # diagnostics only: the contract needs the clocks
+        sampler.start()
 
     heads = args.shard == "heads"
     seed_rank = 0 if heads else rank

@@ -240,15 +240,17 @@ typedef struct {
   const int32_t* append_pos;                 /* [n_requests] (see pi_plan)                      */
   const int32_t* slot_merge;                 /* [n_partial_slots] (see pi_plan); NULL disables
                                                 packinfer_attention_merge                        */
-  uint32_t* sched;                           /* dynamic unit counter of the attention launches:
-                                                each launch resets it on its stream, so one
-                                                attention launch per device plan at a time      */
+  uint32_t* sched;                           /* [2] dynamic unit counter of the attention
+                                                launches and their exit count: zeroed by
+                                                packinfer_plan_upload, left at zero by every
+                                                completed launch (the last CTA resets them), so
+                                                one attention launch per device plan at a time  */
 } pi_device_plan;
 
 /* Enqueue one host->device copy of plan->arena (arena_bytes) into dev_arena (device, >=
  * plan->device_arena_bytes, 256-byte aligned) and one small kernel that expands the row
- * segments into the row table at dev_arena + rows_offset, both on `stream`; fill *out with
- * device pointers into dev_arena.                                                          */
+ * segments into the row table at dev_arena + rows_offset (and zeroes the scheduler counters at
+ * dev_arena + sched_offset), both on `stream`; fill *out with device pointers into dev_arena. */
 PI_API pi_status packinfer_plan_upload(const pi_plan* plan, void* dev_arena, size_t dev_bytes,
                                 pi_stream_t stream, pi_device_plan* out);
 

@@ -108,7 +108,7 @@ struct AttnParams {
   // paged mode (packinfer_attention_decode_paged): K/V tiles straight from the paged cache
   const int32_t* block_table;   // NULL = group-contiguous buffers
   int32_t max_blocks, page, kv_head0;
-  uint32_t* sched;              // dynamic unit counter (zeroed before the launch)
+  uint32_t* sched;              // [0] dynamic unit counter, [1] CTAs exited; zero on entry and on exit
 };
 
 // One paged-mode tile: logical keys [k0, k0 + 128) of block-table row `row` = 128 consecutive slots
@@ -135,6 +135,17 @@ __device__ __forceinline__ void trace_ev(const AttnParams& p, uint32_t tile, int
 // epilogue done).
 __device__ __forceinline__ void trace_unit(const AttnParams& p, uint32_t unit, int ev) {
   if (PI_TRACE && p.trace != nullptr && blockIdx.x == 0 && unit < 64u) p.trace[TRACE_TILES * 32 + unit * 16 + ev] = clock64();
+}
+// Per-CTA %globaltimer (ns) at entry / exit and units processed: trace[TRACE_TILES * 32 + 64 * 16 + 4 * cta + {0, 1, 2}]
+// (load balance / tail of a launch; every CTA)
+constexpr int TRACE_CTA_BASE = TRACE_TILES * 32 + 64 * 16;
+__device__ __forceinline__ void trace_cta(const AttnParams& p, int ev, unsigned long long v) {
+  if (PI_TRACE && p.trace != nullptr) p.trace[TRACE_CTA_BASE + 4 * blockIdx.x + ev] = v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 #ifndef PI_DEC_SLICE
@@ -190,7 +201,11 @@ struct AttnCfg {
   // registers per thread (65536 / THREADS) for the 128-column score row.
   static constexpr int ROLE = 4;
   static constexpr int THREADS = 32 * (ROLE + 8);
-  static constexpr int REG_ROLE = 56, REG_SOFTMAX = 216;   // 128*56 + 256*216 <= 65536
+  static constexpr int REG_ROLE = 56, REG_SOFTMAX = 216;
+  // setmaxnreg.inc blocks until the CTA's pool holds the registers: the pool is the launch
+  // allocation (65536 / THREADS rounded down to 8 per thread = 168), not the register file
+  static_assert(128 * REG_ROLE + 256 * REG_SOFTMAX <= (65536 / (32 * (ROLE + 8)) / 8 * 8) * 32 * (ROLE + 8),
+                "setmaxnreg budget exceeds the launch allocation (the increase would never complete)");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -306,6 +321,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (PI_TRACE && threadIdx.x == 0) trace_cta(p, 0, globaltimer());
   if (threadIdx.x == 0) {
     mbar_init(&bar[B_QFULL], 1);
     mbar_init(&bar[B_QFREE], 1);
@@ -421,6 +437,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
         }
       }
       w = wn;
+      if (PI_TRACE && lane == 0) trace_cta(p, 2, (unsigned long long)(k + 1));   // units taken
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
@@ -550,6 +567,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
                 if (X == 0) {
                   mbar_wait(&bar[B_KFULL0 + ((tt + 1) % C::NSK)], ((tt + 1) / C::NSK) & 1);
                   tc_fence_after();
+                  trace_ev(p, tt, 27);   // pair units: K(j+1) landed as seen by the issuer
                 }
                 issue_s_full(X, tt + 1);
                 trace_ev(p, tt, 2 + 3 * X);
@@ -1402,6 +1420,17 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (PI_TRACE && threadIdx.x == 0) trace_cta(p, 1, globaltimer());
+  if (threadIdx.x == 0) {
+    // self-resetting scheduler: this CTA's producer made its last counter access before the
+    // barrier above; the CTA that exits last returns both counters to zero for the next launch
+    // on the stream (stream order makes the plain stores visible to it)
+    __threadfence();
+    if (atomicAdd(&p.sched[1], 1u) == gridDim.x - 1) {
+      p.sched[0] = 0u;
+      p.sched[1] = 0u;
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -1510,8 +1539,8 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   const int64_t total = (int64_t)p.total_p + (int64_t)p.n_work_d * p.units_d;
   const int grid = (int)std::min<int64_t>(total, num_sms());
   if (p.sched == nullptr) return fail(PI_EINVAL, "device plan has no scheduler counter (packinfer_plan_upload)");
-  s = cuda_check(cudaMemsetAsync(p.sched, 0, sizeof(uint32_t), stream), "scheduler counter reset");
-  if (s != PI_OK) return s;
+  // no reset here: packinfer_plan_upload zeroes the counters and every launch leaves them at zero
+  // (the last CTA to exit resets them), so a launch is one kernel and no memset node
   // kernel instance by the unit kinds present (see get_unit): a prefill-only launch with even r
   // has pair units only, a decode-only launch (or fp32 operands) single-tile units only
   const bool pairs_only = !F32 && p.n_work_d == 0 && (r % 2) == 0;

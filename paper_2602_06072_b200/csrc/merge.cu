@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const pi_merge* __restrict__
   const int m = (int)(gw / hq), h = (int)(gw % hq);
   const pi_merge mg = merges[m];
   float M = -INFINITY;
-  for (int b = lane; b < mg.slot_count; b += 32) M = fmaxf(M, pl[(int64_t)(mg.slot_begin + b) * hq + h]);
+  for (int b = lane; b < mg.slot_count; b += 32) M = fmaxf(M, __ldcg(&pl[(int64_t)(mg.slot_begin + b) * hq + h]));
 #pragma unroll
   for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   constexpr int V = D / 32;
@@ -33,13 +33,32 @@ __global__ void __launch_bounds__(256) merge_kernel(const pi_merge* __restrict__
   for (int i = 0; i < V; ++i) acc[i] = 0.f;
   float W = 0.f;
   if (M != -INFINITY) {
-    for (int b = 0; b < mg.slot_count; ++b) {
-      const int64_t s = mg.slot_begin + b;
-      const float w = expf(pl[s * hq + h] - M);
-      W += w;
-      const float* src = po + (s * hq + h) * D;
+    // slots in batches of MB: every load of a batch is in flight at once (the partials were
+    // written during the attention launch and mostly evicted from L2 by its KV stream, so each
+    // batch is one HBM round trip), then the batch is accumulated in slot order - the same
+    // arithmetic in the same order as the in-kernel merge (packinfer_attention_merge), bitwise
+    constexpr int MB = 4;
+    for (int b0 = 0; b0 < mg.slot_count; b0 += MB) {
+      float lw[MB], x[MB][V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += w * src[lane + 32 * i];
+      for (int q = 0; q < MB; ++q) {
+        if (b0 + q < mg.slot_count) {
+          const int64_t sl = mg.slot_begin + b0 + q;
+          lw[q] = __ldcg(&pl[sl * hq + h]);
+          const float* src = po + (sl * hq + h) * D;
+#pragma unroll
+          for (int i = 0; i < V; ++i) x[q][i] = __ldcg(src + lane + 32 * i);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MB; ++q) {
+        if (b0 + q < mg.slot_count) {
+          const float w = expf(lw[q] - M);
+          W += w;
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] += w * x[q][i];
+        }
+      }
     }
   }
   const float inv = W > 0.f ? 1.f / W : 0.f;

@@ -14,7 +14,10 @@
 namespace pi {
 
 // One CTA per segment (<= 128 rows each, r <= 16 for decode segments): thread j writes row j.
-__global__ void __launch_bounds__(128) expand_rows_kernel(const pi_rowseg* __restrict__ segs, pi_row* __restrict__ rows) {
+// CTA 0 also zeroes the attention launches' scheduler counters (pi_device_plan.sched).
+__global__ void __launch_bounds__(128) expand_rows_kernel(const pi_rowseg* __restrict__ segs, pi_row* __restrict__ rows,
+                                                          uint32_t* __restrict__ sched) {
+  if (blockIdx.x == 0 && threadIdx.x < 2) sched[threadIdx.x] = 0u;
   const pi_rowseg g = segs[blockIdx.x];
   for (int j = threadIdx.x; j < g.count; j += blockDim.x) {
     const bool pre = g.kind == PI_SEG_PREFILL;
@@ -46,10 +49,14 @@ extern "C" pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, si
     return h ? static_cast<const void*>(D + (static_cast<const char*>(h) - H)) : nullptr;
   };
   pi_row* rows = reinterpret_cast<pi_row*>(D + p->rows_offset);
+  uint32_t* sched = reinterpret_cast<uint32_t*>(D + p->sched_offset);
   if (p->n_segs > 0) {
-    pi::expand_rows_kernel<<<p->n_segs, 128, 0, st>>>(static_cast<const pi_rowseg*>(dev(p->segs)), rows);
+    pi::expand_rows_kernel<<<p->n_segs, 128, 0, st>>>(static_cast<const pi_rowseg*>(dev(p->segs)), rows, sched);
     pi_status s = pi::cuda_check(cudaGetLastError(), "expand_rows_kernel launch");
     if (s != PI_OK) return s;
+  } else {
+    e = cudaMemsetAsync(sched, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return pi::fail(PI_ECUDA, std::string("plan upload: ") + cudaGetErrorString(e));
   }
   std::memset(out, 0, sizeof(*out));
   out->copies = static_cast<const pi_copy*>(dev(p->copies));
@@ -67,7 +74,7 @@ extern "C" pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, si
   out->n_partial_slots = p->n_partial_slots;
   out->append_pos = static_cast<const int32_t*>(dev(p->append_pos));
   out->slot_merge = static_cast<const int32_t*>(dev(p->slot_merge));
-  out->sched = reinterpret_cast<uint32_t*>(D + p->sched_offset);
+  out->sched = sched;
   out->buffer_tokens = p->buffer_tokens;
   out->n_requests = p->n_requests;
   out->total_q = p->total_q;

@@ -22,7 +22,7 @@ pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq //
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 TT = 128   # TRACE_TILES in attention.cu
-tr = torch.zeros(TT * 32 + 64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(TT * 32 + 64 * 16 + 4 * 1024, dtype=torch.int64, device="cuda")
 L = pk.lib()
 L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
 L.packinfer_debug_trace(tr.data_ptr())
@@ -31,7 +31,7 @@ torch.cuda.synchronize()
 L.packinfer_debug_trace(None)
 A = tr.cpu().numpy().astype(np.int64)
 a = A[:TT * 32].reshape(TT, 32)
-U = A[TT * 32:].reshape(64, 16)
+U = A[TT * 32:TT * 32 + 64 * 16].reshape(64, 16)
 u0 = U[U > 0].min()
 w = pb.plan.decode_work
 print("unit  mma_waitQ  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done  sm_start sm_gotS0 sm_epi  sm_Oread sm_epidone (n_ktiles rows)")
@@ -53,3 +53,14 @@ print("tile " + " ".join(f"{v:>8s}" for v in names.values()))
 for i in list(range(0, 20)) + list(range(max(20, last - 14), last + 1)):
     base = a[i, 6]
     print(f"{i:4d} " + " ".join(f"{(a[i, e] - base if a[i, e] else -1):8d}" for e in names))
+
+# per-CTA entry / exit (%globaltimer, ns) and units taken: load balance and tail of the traced launch
+C0 = TT * 32 + 64 * 16
+cta = tr.cpu().numpy()[C0:].reshape(-1, 4)
+cta = cta[cta[:, 0] > 0]
+if len(cta):
+    g0 = cta[:, 0].min()
+    st, en = (cta[:, 0] - g0) / 1e3, (cta[:, 1] - g0) / 1e3
+    print(f"CTAs {len(cta)}: entry us max {st.max():.2f}; exit us min {en.min():.2f} median {np.median(en):.2f} "
+          f"p90 {np.percentile(en, 90):.2f} max {en.max():.2f}; units/CTA min {cta[:, 2].min()} max {cta[:, 2].max()}")
+    print("  busy fraction (sum of CTA spans / (CTAs x launch span)):", round(float((en - st).sum() / (len(cta) * en.max())), 3))

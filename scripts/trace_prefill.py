@@ -19,7 +19,7 @@ pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, b.hq //
 out = torch.empty((b.total_q, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
 pb.run(t["q"], t["k_paged"], t["v_paged"], t["block_table"], out)
 TT = 128   # TRACE_TILES in attention.cu
-tr = torch.zeros(TT * 32 + 64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(TT * 32 + 64 * 16 + 4 * 1024, dtype=torch.int64, device="cuda")
 L = pk.lib()
 L.packinfer_debug_trace.argtypes = [ctypes.c_void_p]
 L.packinfer_debug_trace(tr.data_ptr())
@@ -28,7 +28,7 @@ torch.cuda.synchronize()
 L.packinfer_debug_trace(None)
 A = tr.cpu().numpy().astype(np.int64)
 a = A[:TT * 32].reshape(TT, 32)
-U = A[TT * 32:].reshape(64, 16)
+U = A[TT * 32:TT * 32 + 64 * 16].reshape(64, 16)
 t0 = a[a > 0].min()
 names = ["mA_wP", "mA_gotP", "mA_S+", "mB_wP", "mB_gotP", "mB_S+",
          "sA_wS0", "sA_gS0", "sA_PH", "sA_PF", "sB_wS0", "sB_gS0", "sB_PH", "sB_PF", "mA_PV1", "mB_PV1",
@@ -58,3 +58,21 @@ for X, nm in ((0, "A"), (1, "B")):
           f"ldS1+arrive {med(16+2*X, 8+o):.0f}  h1 {med(8+o, 9+o):.0f}")
     fl = a[2:40, 17 + 2 * X]
     print(f"  spec flags (bit0 h0 spec, bit1 h1 spec): {np.bincount((fl & 3).astype(int), minlength=4).tolist()}")
+
+# producer / K-arrival view (events 24 = producer waits K slot, 25 = K TMA issued, 26 = V TMA issued,
+# 27 = issuer saw K(j+1) land; all relative to softmax A's S(j) arrival of the same tile)
+print("tile  Kwait  Kissue  Vissue  K(j+1)seen  mA_PV1  mA_S+   (relative to sA_gS0 of tile j)")
+for i in range(4, 20):
+    r0 = a[i, 7]
+    print(f"{i:4d} " + " ".join(f"{(a[i, c] - r0 if a[i, c] else -1):7d}" for c in (24, 25, 26, 27, 14, 2)))
+
+# per-CTA entry / exit (%globaltimer, ns) and units taken: load balance and tail of the traced launch
+C0 = TT * 32 + 64 * 16
+cta = tr.cpu().numpy()[C0:].reshape(-1, 4)
+cta = cta[cta[:, 0] > 0]
+if len(cta):
+    g0 = cta[:, 0].min()
+    st, en = (cta[:, 0] - g0) / 1e3, (cta[:, 1] - g0) / 1e3
+    print(f"CTAs {len(cta)}: entry us max {st.max():.2f}; exit us min {en.min():.2f} median {np.median(en):.2f} "
+          f"p90 {np.percentile(en, 90):.2f} max {en.max():.2f}; units/CTA min {cta[:, 2].min()} max {cta[:, 2].max()}")
+    print("  busy fraction (sum of CTA spans / (CTAs x launch span)):", round(float((en - st).sum() / (len(cta) * en.max())), 3))
