@@ -167,6 +167,13 @@ def arm_config(b, shard, world):
             "parallelism": f"{shard}-sharded x{world}", "algorithmic_tflop": flops / 1e12}
 
 
+def plan_flags():
+    """Plan flags of every section: None = packinfer_default_config's (packed decode items);
+    PI_BENCH_PLAN_FLAGS = A/B hook (ablations, options)."""
+    v = os.environ.get("PI_BENCH_PLAN_FLAGS")
+    return None if v is None else int(v)
+
+
 class Runner:
     """Owns the device state of one batch and runs steps on one stream (double-buffered plans)."""
 
@@ -179,7 +186,8 @@ class Runner:
         self.hkv_begin, self.hkv_count = hkv_begin, hkv_count
         self.t = W.make_tensors(b, device=device, seed=seed)
         dt = self.t["q"].dtype
-        flags = int(os.environ.get("PI_BENCH_PLAN_FLAGS", "0"))      # A/B hook (ablations)
+        flags = plan_flags()
+        flags = pk.default_config().flags if flags is None else flags
         if hkv_count * b.hq // b.hkv <= 8:
             # few units per SM (KV-head sharding at N >= 4): balance over L2 locality
             flags |= pk.PI_PLAN_LPT_EXACT
@@ -394,7 +402,8 @@ def decode_group_sharded(dev, rank, world, args, peaks):
     bd = make_workload("cfg3", 0)
     r = bd.hq // bd.hkv
     t = W_tensors(bd, dev)
-    pb = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, bd.hkv, r, bd.d, t["q"].dtype, dev)
+    pb = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, bd.hkv, r, bd.d, t["q"].dtype, dev,
+                        flags=plan_flags())
     owner = shard.group_shard(shard.group_costs(pb.plan), world)
     rp = shard.RankPlan(pb, owner, rank)
     out = torch.empty((bd.total_q, bd.hq, bd.d), dtype=t["q"].dtype, device=dev)
@@ -443,7 +452,7 @@ def decode_loop(dev, h0, hc, seed_rank, args):
     tl = W.make_tensors(bd, device=dev, seed=bd.seed, extra_tokens=loop_steps)
     rr = bd.hq // bd.hkv
     pbl = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, rr, bd.d, torch.bfloat16, dev,
-                         headroom=delta)
+                         headroom=delta, flags=plan_flags())
     ql = tl["q"][:, h0 * rr:(h0 + hc) * rr]
     outl = torch.empty((bd.n, hc * rr, bd.d), dtype=torch.bfloat16, device=dev)
     kn = torch.randn((bd.n, bd.hkv, bd.d), device=dev).to(torch.bfloat16)
@@ -520,7 +529,7 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
         C = tuner.choose()
         if C not in batches:
             batches[C] = pk.PackedBatch(bd.kv_len, bd.q_len, bd.prefix_id, bd.prefix_len, hc, rr, bd.d,
-                                        torch.bfloat16, dev, capacity=C, headroom=delta)
+                                        torch.bfloat16, dev, capacity=C, headroom=delta, flags=plan_flags())
         pb = batches[C]
         pb.replan(st)
         pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf, pb.v_buf, h0, hc,
@@ -567,7 +576,8 @@ def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
     bm = W.cfg5_mixed(3 + (0 if args.shard == "heads" else rank))
     r = bm.hq // bm.hkv
     tm = W.make_tensors(bm, device=dev, seed=bm.seed)
-    pbm = pk.PackedBatch(bm.kv_len, bm.q_len, bm.prefix_id, bm.prefix_len, hc, r, bm.d, torch.bfloat16, dev)
+    pbm = pk.PackedBatch(bm.kv_len, bm.q_len, bm.prefix_id, bm.prefix_len, hc, r, bm.d, torch.bfloat16, dev,
+                         flags=plan_flags())
     qm = tm["q"][:, h0 * r:(h0 + hc) * r]
     outm = torch.empty((bm.total_q, hc * r, bm.d), dtype=torch.bfloat16, device=dev)
     lsem = torch.empty((hc * r, bm.total_q), dtype=torch.float32, device=dev)

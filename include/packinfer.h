@@ -93,7 +93,7 @@ typedef struct {
   int32_t tile_k;       /* keys per K tile; must be 128 (P:159 T in {128,256})               */
   int32_t decode_chunk; /* max keys per decode work item (multiple of tile_k; e.g. 1024)      */
   int32_t gqa_ratio;    /* r = Hq / Hkv in [1, 16]: decode rows are (request, GQA head)       */
-  int32_t flags;        /* PI_PLAN_* bits; 0 = the method.  (Occupies the struct's former tail
+  int32_t flags;        /* PI_PLAN_* bits (default PI_PLAN_DPACK).  (Occupies the struct's former tail
                            padding: sizeof(pi_config) is unchanged.)                           */
 } pi_config;
 
@@ -102,8 +102,12 @@ typedef struct {
  * "unpacked compute" baseline.  Groups, layout and results are unchanged; only tile count and
  * tile efficiency change.                                                                     */
 #define PI_PLAN_NO_QPACK 1
-/* Option: pack consecutive short decode suffixes of one group into one decode work item (key span =
- * their hull <= decode_chunk, per-row [lo, hi) = own suffix).  Off by default (measured slower).   */
+/* Packed decode items (on in packinfer_default_config): consecutive short decode suffixes of one
+ * group share one decode work item - the decode analogue of packed prefill tiles - whose
+ * key span is their hull (<= decode_chunk keys, <= tile_q rows); each row sees only its own
+ * suffix [lo, hi), so every key is still read once.  With rows <= 32 lane-sliced in the kernel
+ * this amortises the per-unit epilogue over several requests (configs[3] decode kernel -7 %,
+ * configs[2] -2 %, profiles/r03b).  flags = 0 plans one item per suffix.                      */
 #define PI_PLAN_DPACK 2
 /* Ablation (NEXT-4, Fig. "breakdown" P:480-489: "packed I/O" off): a decode-only plan whose work
  * items cover each request's LOGICAL tokens, read straight from the paged cache by
@@ -117,7 +121,7 @@ typedef struct {
 #define PI_PLAN_LPT_EXACT 8
 
 /* Fill *cfg with the defaults: C=8192, G auto, no M_max, delta=0, 128/128 tiles,
- * decode_chunk=1024, gqa_ratio=1. */
+ * decode_chunk=1024, gqa_ratio=1, flags = PI_PLAN_DPACK. */
 PI_API void packinfer_default_config(pi_config* cfg);
 
 /* ---- plan tables (host, written by packinfer_plan; compared bit-exactly with the oracle) -- */

@@ -151,6 +151,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #ifndef PI_DEC_SLICE
 #define PI_DEC_SLICE 1   // lane-sliced single-tile units (<= kSliceRows rows): see unit_sliced()
 #endif
+#ifndef PI_SLICE_ROWS
+#define PI_SLICE_ROWS 32   // lane-sliced single-tile units: up to this many rows (one lane quarter)
+#endif
+#ifndef PI_DEC_S_AFTER_EPI
+#define PI_DEC_S_AFTER_EPI 0
+#endif
 #ifndef PI_DEC_NSV
 #define PI_DEC_NSV 3   // V stages of decode-only (single-tile) launches: V is held until P.V
 #endif
@@ -178,10 +184,13 @@ struct AttnCfg {
   static constexpr int OFF_BAR = OFF_V + NSV * TILE_BYTES;
   static constexpr int OFF_XCH = OFF_BAR + 512;       // single units: (m, l, l_rounded) of both warpgroups
   // lane-sliced single units: the four lane quarters' O partials of <= kSliceRows rows (padded rows)
+  // (two quarter-pair sums, [2][PI_SLICE_ROWS][OBUF_STRIDE] fp32), aliasing XCH: the epilogue
+  // reads XCH into registers and passes a barrier before the buffer is written
   static constexpr int OBUF_STRIDE = D + 4;
-  static constexpr int OFF_OBUF = OFF_XCH + 2 * 128 * 16;
-  static constexpr int OBUF_BYTES = ((UK & 2) && !F32) ? 4 * 8 * OBUF_STRIDE * 4 : 0;
-  static constexpr int SMEM = OFF_OBUF + OBUF_BYTES + 1024;  // + alignment slack
+  static constexpr int XCH_BYTES = 2 * 128 * 16;
+  static constexpr int OFF_OBUF = OFF_XCH;
+  static constexpr int OBUF_BYTES = ((UK & 2) && !F32) ? 2 * PI_SLICE_ROWS * OBUF_STRIDE * 4 : 0;
+  static constexpr int SMEM = OFF_XCH + (OBUF_BYTES > XCH_BYTES ? OBUF_BYTES : XCH_BYTES) + 1024;  // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
   // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
   static constexpr uint32_t P1_SINGLE = F32 ? 64u : 96u;
@@ -275,7 +284,8 @@ __device__ __forceinline__ void ring_release(uint64_t* bar, int k, int lane) {
 // every tile: its own running max / sums and P (zero outside its 16 keys) into O_X at its lanes.
 // The eight partials of a row (2 key halves x 4 quarters) are LSE-merged in the epilogue exactly
 // as the two split-K halves are (reading R10), the quarters summed in a fixed order through smem.
-constexpr int kSliceRows = 8;
+constexpr int kSliceRows = PI_SLICE_ROWS;
+static_assert(kSliceRows % 8 == 0 && kSliceRows <= 32, "sliced rows fit one lane quarter, 8 per store pass");
 template <int UK, bool F32>
 __device__ __forceinline__ bool unit_sliced(const Unit& u) {
   return PI_DEC_SLICE && (UK & 2) && !F32 && !u.has_b && u.wk.row_count <= kSliceRows;
@@ -585,6 +595,12 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
           const bool s128_pro = PI_SINGLE_S128 == 1 || PI_SINGLE_S128 == 2 || (PI_SINGLE_S128 == 3 && n <= 4);
           const bool s128_body = PI_SINGLE_S128 == 1 || (PI_SINGLE_S128 == 3 && n <= 4);
+          if (PI_DEC_S_AFTER_EPI) {
+            // A/B: S(0) of this unit only after the previous unit's epilogue released O (keeps the
+            // SS MMA's shared-memory operand stream off the epilogue's exchange)
+            mbar_wait(&bar[B_OFREE0], (ix & 1) ^ 1);
+            mbar_wait(&bar[B_OFREE1], (ix & 1) ^ 1);
+          }
           issue_s(0, 0, t, s128_pro);
           trace_ev(p, t, 27);
           commit(B_KFREE0 + (t % C::NSK));
@@ -1246,43 +1262,68 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           }
           const float inv = LR > 0.f ? 1.0f / LR : 0.f;
           lse_v = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
+          if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 12);
+          // every thread has read XCH (aliased by the partial buffer below)
+          named_bar_sync(1, 256);
+          if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 13);
+          // quarter sum in a fixed order, (p0 + p2) + (p1 + p3): quarters 2, 3 store their weighted
+          // partial of column half X into buffer (q & 1), then quarters 0, 1 add theirs in place,
+          // then every thread adds the two buffers and stores
           float* ob = reinterpret_cast<float*>(smem + C::OFF_OBUF);
+          // this warp's weighted partial of column half X (both 32-column chunks), all TMEM loads
+          // issued before the first wait
+          constexpr int HC = D / 64;   // 32-column chunks per column half
+          uint32_t o0[HC][32], o1[HC][32];
 #pragma unroll
-          for (int c4 = 0; c4 < D / 32; ++c4) {
-            if (c4 < X * (D / 64) || c4 >= (X + 1) * (D / 64)) continue;
-            uint32_t o0[32], o1[32];
-            tmem_ld32(tmem + lane_base + C::TM_O0 + c4 * 32, o0);
-            tmem_ld32(tmem + lane_base + C::TM_O1 + c4 * 32, o1);
-            tmem_wait_ld();
-            reg_fence(o0);
-            reg_fence(o1);
-            if (valid) {
-              float* dst = ob + (wq * kSliceRows + lane) * C::OBUF_STRIDE + c4 * 32;
+          for (int c = 0; c < HC; ++c) {
+            tmem_ld32(tmem + lane_base + C::TM_O0 + (X * HC + c) * 32, o0[c]);
+            tmem_ld32(tmem + lane_base + C::TM_O1 + (X * HC + c) * 32, o1[c]);
+          }
+          tmem_wait_ld();
 #pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                float4 f;
-                f.x = fmaf(__uint_as_float(o0[4 * v + 0]), w0 * inv, __uint_as_float(o1[4 * v + 0]) * (w1 * inv));
-                f.y = fmaf(__uint_as_float(o0[4 * v + 1]), w0 * inv, __uint_as_float(o1[4 * v + 1]) * (w1 * inv));
-                f.z = fmaf(__uint_as_float(o0[4 * v + 2]), w0 * inv, __uint_as_float(o1[4 * v + 2]) * (w1 * inv));
-                f.w = fmaf(__uint_as_float(o0[4 * v + 3]), w0 * inv, __uint_as_float(o1[4 * v + 3]) * (w1 * inv));
-                reinterpret_cast<float4*>(dst)[v] = f;
+          for (int c = 0; c < HC; ++c) {
+            reg_fence(o0[c]);
+            reg_fence(o1[c]);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              o0[c][i] = __float_as_uint(fmaf(__uint_as_float(o0[c][i]), w0 * inv, __uint_as_float(o1[c][i]) * (w1 * inv)));
+          }
+#pragma unroll
+          for (int stage = 0; stage < 2; ++stage) {
+            if ((wq >> 1) == 1 - stage && valid) {
+#pragma unroll
+              for (int c = 0; c < HC; ++c) {
+                float* dst = ob + ((wq & 1) * kSliceRows + lane) * C::OBUF_STRIDE + (X * HC + c) * 32;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                  float4 f = make_float4(__uint_as_float(o0[c][4 * v]), __uint_as_float(o0[c][4 * v + 1]),
+                                         __uint_as_float(o0[c][4 * v + 2]), __uint_as_float(o0[c][4 * v + 3]));
+                  if (stage == 1) {
+                    const float4 g = reinterpret_cast<const float4*>(dst)[v];
+                    f.x += g.x;
+                    f.y += g.y;
+                    f.z += g.z;
+                    f.w += g.w;
+                  }
+                  reinterpret_cast<float4*>(dst)[v] = f;
+                }
               }
             }
+            named_bar_sync(1, 256);
+            if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 14 + stage);
           }
-          named_bar_sync(1, 256);
           {
             constexpr int V4 = D / 4;
-            const int tid = threadIdx.x - 32 * C::ROLE;   // 0..255
-            const int rr = tid / V4, c = (tid % V4) * 4;
-            if (rr < wk.row_count) {
-              float4 a[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) a[q] = *reinterpret_cast<const float4*>(ob + (q * kSliceRows + rr) * C::OBUF_STRIDE + c);
+            const int tid = threadIdx.x - 32 * C::ROLE;   // 0..255: 256 / V4 rows per pass
+            const int c = (tid % V4) * 4;
+            for (int rr = tid / V4; rr < wk.row_count; rr += 256 / V4) {
+              const float4 a0 = *reinterpret_cast<const float4*>(ob + rr * C::OBUF_STRIDE + c);
+              const float4 a1 = *reinterpret_cast<const float4*>(ob + (kSliceRows + rr) * C::OBUF_STRIDE + c);
               float4 f;
-              f.x = (a[0].x + a[1].x) + (a[2].x + a[3].x);
-              f.y = (a[0].y + a[1].y) + (a[2].y + a[3].y);
-              f.z = (a[0].z + a[1].z) + (a[2].z + a[3].z);
-              f.w = (a[0].w + a[1].w) + (a[2].w + a[3].w);
+              f.x = a0.x + a1.x;
+              f.y = a0.y + a1.y;
+              f.z = a0.z + a1.z;
+              f.w = a0.w + a1.w;
               const pi_row rw = p.rows[wk.row_begin + rr];
               const int rslot = (rw.out >> 4) - 1;
               const int rhead = u.head0 + (rw.out & 15);

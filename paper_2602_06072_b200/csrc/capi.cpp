@@ -52,7 +52,7 @@ void packinfer_default_config(pi_config* cfg) {
   cfg->tile_k = 128;
   cfg->decode_chunk = 1024;
   cfg->gqa_ratio = 1;
-  cfg->flags = 0;
+  cfg->flags = PI_PLAN_DPACK;   // packed decode items (measured faster since lane slicing covers <= 32 rows)
 }
 
 pi_status packinfer_plan(int32_t n, const int32_t* kv_len, const int32_t* q_len,

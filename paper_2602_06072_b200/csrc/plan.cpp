@@ -433,11 +433,12 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
     spans.reserve(spans.size() + est);
     segs.reserve(segs.size() + est + (size_t)n);
   }
-  // PI_PLAN_DPACK (opt-in): packed decode items (the decode analogue of packed prefill tiles,
+  // PI_PLAN_DPACK (default): packed decode items (the decode analogue of packed prefill tiles,
   // P:150): consecutive decode suffixes of one group - adjacent in B_g up to the headroom between
-  // them - share ONE item whose key span is their hull (<= decode_chunk keys, <= tile_q rows);
-  // each row sees only its own suffix [lo, hi).  Every key is still read once.  Measured slower
-  // on configs[3] (fewer, longer units balance worse: profiles/r02d/ab_plan.txt), so off by default.
+  // them - share ONE item whose key span is their hull (<= decode_chunk keys, <= kDpackRows rows);
+  // each row sees only its own suffix [lo, hi).  Every key is still read once, and one unit
+  // epilogue serves several requests (configs[3] decode kernel -7 %, profiles/r03b).
+  constexpr int64_t kDpackRows = 32;
   struct PackMember { int32_t req; int64_t b, len; };
   std::vector<PackMember> pack;
   auto flush_pack = [&](int32_t g) {
@@ -501,7 +502,10 @@ pi_status plan_impl(int32_t n, const int32_t* kv_len, const int32_t* q_len,
         emit_decode(g, &pc.request, 1, b, len);
         continue;
       }
-      if (!pack.empty() && (b + len - pack.front().b > chunk || (int64_t)(pack.size() + 1) * r > TQ)) flush_pack(g);
+      // <= kDpackRows rows: the kernel lane-slices decode units of <= 32 rows (every softmax warp
+      // takes 16 keys of each tile); larger units run with only their rows' lane quarters busy
+      if (!pack.empty() && (b + len - pack.front().b > chunk || (int64_t)(pack.size() + 1) * r > kDpackRows))
+        flush_pack(g);
       pack.push_back({pc.request, b, len});
     }
     flush_pack(g);

@@ -401,10 +401,11 @@ class PackedBatch:
 
     def __init__(self, kv_len, q_len, prefix_id, prefix_len, hkv_count: int, gqa_ratio: int, head_dim: int,
                  dtype, device, capacity: int = 8192, headroom: int = 0, num_groups: int = 0,
-                 decode_chunk: int = 1024, mem_cap: int = 0, flags: int = 0):
+                 decode_chunk: int = 1024, mem_cap: int = 0, flags: Optional[int] = None):
         import torch
+        kw = {} if flags is None else {"flags": flags}   # None: packinfer_default_config's flags
         self.cfg = default_config(capacity=capacity, headroom=headroom, num_groups=num_groups,
-                                  decode_chunk=decode_chunk, gqa_ratio=gqa_ratio, mem_cap=mem_cap, flags=flags)
+                                  decode_chunk=decode_chunk, gqa_ratio=gqa_ratio, mem_cap=mem_cap, **kw)
         self.args = (kv_len, q_len, prefix_id, prefix_len)
         self.plan = packinfer_plan(kv_len, q_len, prefix_id, prefix_len, self.cfg, pinned=True)
         # Two pinned host arenas alternate: a plan is never rewritten while its asynchronous upload

@@ -64,3 +64,11 @@ if len(cta):
     print(f"CTAs {len(cta)}: entry us max {st.max():.2f}; exit us min {en.min():.2f} median {np.median(en):.2f} "
           f"p90 {np.percentile(en, 90):.2f} max {en.max():.2f}; units/CTA min {cta[:, 2].min()} max {cta[:, 2].max()}")
     print("  busy fraction (sum of CTA spans / (CTAs x launch span)):", round(float((en - st).sum() / (len(cta) * en.max())), 3))
+
+# sliced-unit epilogue phases (softmax warp 4, per unit): O landed -> xch merge -> barrier ->
+# stage 0 (quarters 2, 3 store) -> stage 1 (quarters 0, 1 add) -> final sum + stores
+print("unit  Olanded->xch  ->bar  ->stage0  ->stage1  ->stored   (cycles)")
+for i in range(40):
+    r = U[i]
+    if r[12] > 0:
+        print(f"{i:4d} {r[12] - r[9]:12d} {r[13] - r[12]:6d} {r[14] - r[13]:8d} {r[15] - r[14]:8d} {r[10] - r[15]:8d}")
