@@ -189,7 +189,9 @@ struct AttnCfg {
   static constexpr int OBUF_STRIDE = D + 4;
   static constexpr int XCH_BYTES = 2 * 128 * 16;
   static constexpr int OFF_OBUF = OFF_XCH;
-  static constexpr int OBUF_BYTES = ((UK & 2) && !F32) ? 2 * PI_SLICE_ROWS * OBUF_STRIDE * 4 : 0;
+  // (or, for units of <= 8 rows, the eight raw partials [8][8][OBUF_STRIDE] + their (m, l, l_r))
+  static constexpr int OBUF_ROWS = 2 * PI_SLICE_ROWS > 64 ? 2 * PI_SLICE_ROWS : 64;
+  static constexpr int OBUF_BYTES = ((UK & 2) && !F32) ? OBUF_ROWS * OBUF_STRIDE * 4 : 0;
   static constexpr int SMEM = OFF_XCH + (OBUF_BYTES > XCH_BYTES ? OBUF_BYTES : XCH_BYTES) + 1024;  // + alignment slack
   // single units: warpgroup B writes P of keys 64..127 over the S columns it has read itself
   // (bf16: 32 packed columns at 96..127; fp32: 64 columns at 64..127), never over warpgroup A's
@@ -285,6 +287,7 @@ __device__ __forceinline__ void ring_release(uint64_t* bar, int k, int lane) {
 // The eight partials of a row (2 key halves x 4 quarters) are LSE-merged in the epilogue exactly
 // as the two split-K halves are (reading R10), the quarters summed in a fixed order through smem.
 constexpr int kSliceRows = PI_SLICE_ROWS;
+constexpr int kSliceFast = 8;   // sliced units of <= 8 rows: one-barrier epilogue (8 raw partials in smem)
 static_assert(kSliceRows % 8 == 0 && kSliceRows <= 32, "sliced rows fit one lane quarter, 8 per store pass");
 template <int UK, bool F32>
 __device__ __forceinline__ bool unit_sliced(const Unit& u) {
@@ -1236,94 +1239,78 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       int c4_begin = 0, c4_end = D / 32;
       if constexpr ((UK & 2) && !F32) {
         if (sl) {
-          // lane-sliced unit: merge the row's eight partials (key half X' x lane quarter q, reading
-          // R10), scale this quarter's O_0 / O_1 into the smem partial of quarter wq, then sum the
-          // four quarters in a fixed order (bitwise reproducible) and store.
-          float4* xch = reinterpret_cast<float4*>(smem + C::OFF_XCH);
-          xch[X * 128 + row_id] = make_float4(m_ref, l, lr, 0.f);
-          named_bar_sync(1, 256);
-          float M = NEG_INF, mq[8], lq[8], rq[8];
+          if (wk.row_count <= kSliceFast) {
+            // <= 8 rows (one request, or a few packed ones): ONE barrier.  Every warp stores its
+            // quarter's raw partials O_0 / O_1 (column half X) and its own (m, l, l_rounded) in the
+            // row's padding; then each thread merges the eight partials of one row and 4 columns
+            // (reading R10, fixed order k = 0..7) and stores.
+            float* pb = reinterpret_cast<float*>(smem + C::OFF_OBUF);   // [8 partials][kSliceFast rows][OBUF_STRIDE]
+            constexpr int HC = D / 64;
+            uint32_t o0[HC][32], o1[HC][32];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float4 o = xch[(k >> 2) * 128 + (k & 3) * 32 + lane];
-            mq[k] = o.x;
-            lq[k] = o.y;
-            rq[k] = o.z;
-            if (o.y > 0.f) M = fmaxf(M, o.x);
-          }
-          float L = 0.f, LR = 0.f, w0 = 0.f, w1 = 0.f;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float wk_ = lq[k] > 0.f ? ex2(mq[k] - M) : 0.f;
-            L += lq[k] * wk_;
-            LR += rq[k] * wk_;
-            if (k == wq) w0 = wk_;
-            if (k == 4 + wq) w1 = wk_;
-          }
-          const float inv = LR > 0.f ? 1.0f / LR : 0.f;
-          lse_v = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
-          if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 12);
-          // every thread has read XCH (aliased by the partial buffer below)
-          named_bar_sync(1, 256);
-          if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 13);
-          // quarter sum in a fixed order, (p0 + p2) + (p1 + p3): quarters 2, 3 store their weighted
-          // partial of column half X into buffer (q & 1), then quarters 0, 1 add theirs in place,
-          // then every thread adds the two buffers and stores
-          float* ob = reinterpret_cast<float*>(smem + C::OFF_OBUF);
-          // this warp's weighted partial of column half X (both 32-column chunks), all TMEM loads
-          // issued before the first wait
-          constexpr int HC = D / 64;   // 32-column chunks per column half
-          uint32_t o0[HC][32], o1[HC][32];
-#pragma unroll
-          for (int c = 0; c < HC; ++c) {
-            tmem_ld32(tmem + lane_base + C::TM_O0 + (X * HC + c) * 32, o0[c]);
-            tmem_ld32(tmem + lane_base + C::TM_O1 + (X * HC + c) * 32, o1[c]);
-          }
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < HC; ++c) {
-            reg_fence(o0[c]);
-            reg_fence(o1[c]);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              o0[c][i] = __float_as_uint(fmaf(__uint_as_float(o0[c][i]), w0 * inv, __uint_as_float(o1[c][i]) * (w1 * inv)));
-          }
-#pragma unroll
-          for (int stage = 0; stage < 2; ++stage) {
-            if ((wq >> 1) == 1 - stage && valid) {
+            for (int c = 0; c < HC; ++c) {
+              tmem_ld32(tmem + lane_base + C::TM_O0 + (X * HC + c) * 32, o0[c]);
+              tmem_ld32(tmem + lane_base + C::TM_O1 + (X * HC + c) * 32, o1[c]);
+            }
+            tmem_wait_ld();
+            if (valid) {
+              float* d0 = pb + (wq * kSliceFast + lane) * C::OBUF_STRIDE;         // partial k = wq (key half 0)
+              float* d1 = pb + ((4 + wq) * kSliceFast + lane) * C::OBUF_STRIDE;   // partial k = 4 + wq (key half 1)
 #pragma unroll
               for (int c = 0; c < HC; ++c) {
-                float* dst = ob + ((wq & 1) * kSliceRows + lane) * C::OBUF_STRIDE + (X * HC + c) * 32;
+                reg_fence(o0[c]);
+                reg_fence(o1[c]);
 #pragma unroll
                 for (int v = 0; v < 8; ++v) {
-                  float4 f = make_float4(__uint_as_float(o0[c][4 * v]), __uint_as_float(o0[c][4 * v + 1]),
-                                         __uint_as_float(o0[c][4 * v + 2]), __uint_as_float(o0[c][4 * v + 3]));
-                  if (stage == 1) {
-                    const float4 g = reinterpret_cast<const float4*>(dst)[v];
-                    f.x += g.x;
-                    f.y += g.y;
-                    f.z += g.z;
-                    f.w += g.w;
-                  }
-                  reinterpret_cast<float4*>(dst)[v] = f;
+                  const int col = (X * HC + c) * 32 + 4 * v;
+                  *reinterpret_cast<float4*>(d0 + col) =
+                      make_float4(__uint_as_float(o0[c][4 * v]), __uint_as_float(o0[c][4 * v + 1]),
+                                  __uint_as_float(o0[c][4 * v + 2]), __uint_as_float(o0[c][4 * v + 3]));
+                  *reinterpret_cast<float4*>(d1 + col) =
+                      make_float4(__uint_as_float(o1[c][4 * v]), __uint_as_float(o1[c][4 * v + 1]),
+                                  __uint_as_float(o1[c][4 * v + 2]), __uint_as_float(o1[c][4 * v + 3]));
                 }
               }
+              // this warp's softmax state is partial k = 4 X + wq
+              float* ds = pb + ((4 * X + wq) * kSliceFast + lane) * C::OBUF_STRIDE + D;
+              ds[0] = m_ref;
+              ds[1] = l;
+              ds[2] = lr;
             }
             named_bar_sync(1, 256);
-            if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 14 + stage);
-          }
-          {
+            if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 12);
             constexpr int V4 = D / 4;
-            const int tid = threadIdx.x - 32 * C::ROLE;   // 0..255: 256 / V4 rows per pass
-            const int c = (tid % V4) * 4;
-            for (int rr = tid / V4; rr < wk.row_count; rr += 256 / V4) {
-              const float4 a0 = *reinterpret_cast<const float4*>(ob + rr * C::OBUF_STRIDE + c);
-              const float4 a1 = *reinterpret_cast<const float4*>(ob + (kSliceRows + rr) * C::OBUF_STRIDE + c);
-              float4 f;
-              f.x = a0.x + a1.x;
-              f.y = a0.y + a1.y;
-              f.z = a0.z + a1.z;
-              f.w = a0.w + a1.w;
+            static_assert(256 / V4 >= kSliceFast, "one pass of the merge covers every row");
+            const int tid = threadIdx.x - 32 * C::ROLE;
+            const int rr = tid / V4, c = (tid % V4) * 4;
+            if (rr < wk.row_count) {
+              float mq[8], lq[8], rq[8], Mx = NEG_INF;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float* st = pb + (k * kSliceFast + rr) * C::OBUF_STRIDE + D;
+                mq[k] = st[0];
+                lq[k] = st[1];
+                rq[k] = st[2];
+                if (lq[k] > 0.f) Mx = fmaxf(Mx, mq[k]);
+              }
+              float L = 0.f, LR = 0.f, wq8[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                wq8[k] = lq[k] > 0.f ? ex2(mq[k] - Mx) : 0.f;
+                L += lq[k] * wq8[k];
+                LR += rq[k] * wq8[k];
+              }
+              const float inv = LR > 0.f ? 1.0f / LR : 0.f;
+              float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float wk_ = wq8[k] * inv;
+                const float4 a = *reinterpret_cast<const float4*>(pb + (k * kSliceFast + rr) * C::OBUF_STRIDE + c);
+                f.x = fmaf(a.x, wk_, f.x);
+                f.y = fmaf(a.y, wk_, f.y);
+                f.z = fmaf(a.z, wk_, f.z);
+                f.w = fmaf(a.w, wk_, f.w);
+              }
               const pi_row rw = p.rows[wk.row_begin + rr];
               const int rslot = (rw.out >> 4) - 1;
               const int rhead = u.head0 + (rw.out & 15);
@@ -1338,13 +1325,126 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
               } else {
                 *reinterpret_cast<float4*>(p.partial_o + ((int64_t)rslot * p.hq_count + rhead) * D + c) = f;
               }
+              if (c == 0) {
+                const float lv = L > 0.f ? (Mx + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
+                if (rslot < 0) {
+                  if (p.lse) p.lse[(int64_t)rhead * p.total_q + rw.q_token] = lv;
+                } else {
+                  p.partial_lse[(int64_t)rslot * p.hq_count + rhead] = lv;
+                }
+              }
             }
-          }
-          if (valid && X == 0 && wq == 0) {
-            if (slot < 0) {
-              if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
-            } else {
-              p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
+          } else {
+            // lane-sliced unit: merge the row's eight partials (key half X' x lane quarter q, reading
+            // R10), scale this quarter's O_0 / O_1 into the smem partial of quarter wq, then sum the
+            // four quarters in a fixed order (bitwise reproducible) and store.
+            float4* xch = reinterpret_cast<float4*>(smem + C::OFF_XCH);
+            xch[X * 128 + row_id] = make_float4(m_ref, l, lr, 0.f);
+            named_bar_sync(1, 256);
+            float M = NEG_INF, mq[8], lq[8], rq[8];
+  #pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float4 o = xch[(k >> 2) * 128 + (k & 3) * 32 + lane];
+              mq[k] = o.x;
+              lq[k] = o.y;
+              rq[k] = o.z;
+              if (o.y > 0.f) M = fmaxf(M, o.x);
+            }
+            float L = 0.f, LR = 0.f, w0 = 0.f, w1 = 0.f;
+  #pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float wk_ = lq[k] > 0.f ? ex2(mq[k] - M) : 0.f;
+              L += lq[k] * wk_;
+              LR += rq[k] * wk_;
+              if (k == wq) w0 = wk_;
+              if (k == 4 + wq) w1 = wk_;
+            }
+            const float inv = LR > 0.f ? 1.0f / LR : 0.f;
+            lse_v = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : NEG_INF;
+            if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 12);
+            // every thread has read XCH (aliased by the partial buffer below)
+            named_bar_sync(1, 256);
+            if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 13);
+            // quarter sum in a fixed order, (p0 + p2) + (p1 + p3): quarters 2, 3 store their weighted
+            // partial of column half X into buffer (q & 1), then quarters 0, 1 add theirs in place,
+            // then every thread adds the two buffers and stores
+            float* ob = reinterpret_cast<float*>(smem + C::OFF_OBUF);
+            // this warp's weighted partial of column half X (both 32-column chunks), all TMEM loads
+            // issued before the first wait
+            constexpr int HC = D / 64;   // 32-column chunks per column half
+            uint32_t o0[HC][32], o1[HC][32];
+  #pragma unroll
+            for (int c = 0; c < HC; ++c) {
+              tmem_ld32(tmem + lane_base + C::TM_O0 + (X * HC + c) * 32, o0[c]);
+              tmem_ld32(tmem + lane_base + C::TM_O1 + (X * HC + c) * 32, o1[c]);
+            }
+            tmem_wait_ld();
+  #pragma unroll
+            for (int c = 0; c < HC; ++c) {
+              reg_fence(o0[c]);
+              reg_fence(o1[c]);
+  #pragma unroll
+              for (int i = 0; i < 32; ++i)
+                o0[c][i] = __float_as_uint(fmaf(__uint_as_float(o0[c][i]), w0 * inv, __uint_as_float(o1[c][i]) * (w1 * inv)));
+            }
+  #pragma unroll
+            for (int stage = 0; stage < 2; ++stage) {
+              if ((wq >> 1) == 1 - stage && valid) {
+  #pragma unroll
+                for (int c = 0; c < HC; ++c) {
+                  float* dst = ob + ((wq & 1) * kSliceRows + lane) * C::OBUF_STRIDE + (X * HC + c) * 32;
+  #pragma unroll
+                  for (int v = 0; v < 8; ++v) {
+                    float4 f = make_float4(__uint_as_float(o0[c][4 * v]), __uint_as_float(o0[c][4 * v + 1]),
+                                           __uint_as_float(o0[c][4 * v + 2]), __uint_as_float(o0[c][4 * v + 3]));
+                    if (stage == 1) {
+                      const float4 g = reinterpret_cast<const float4*>(dst)[v];
+                      f.x += g.x;
+                      f.y += g.y;
+                      f.z += g.z;
+                      f.w += g.w;
+                    }
+                    reinterpret_cast<float4*>(dst)[v] = f;
+                  }
+                }
+              }
+              named_bar_sync(1, 256);
+              if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 14 + stage);
+            }
+            {
+              constexpr int V4 = D / 4;
+              const int tid = threadIdx.x - 32 * C::ROLE;   // 0..255: 256 / V4 rows per pass
+              const int c = (tid % V4) * 4;
+              for (int rr = tid / V4; rr < wk.row_count; rr += 256 / V4) {
+                const float4 a0 = *reinterpret_cast<const float4*>(ob + rr * C::OBUF_STRIDE + c);
+                const float4 a1 = *reinterpret_cast<const float4*>(ob + (kSliceRows + rr) * C::OBUF_STRIDE + c);
+                float4 f;
+                f.x = a0.x + a1.x;
+                f.y = a0.y + a1.y;
+                f.z = a0.z + a1.z;
+                f.w = a0.w + a1.w;
+                const pi_row rw = p.rows[wk.row_begin + rr];
+                const int rslot = (rw.out >> 4) - 1;
+                const int rhead = u.head0 + (rw.out & 15);
+                if (rslot < 0) {
+                  if (!p.out_f32) {
+                    uint8_t* dst = p.out + ((int64_t)rw.q_token * p.out_row_stride + (int64_t)rhead * D + c) * 2;
+                    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(f.x, f.y), pack_bf16(f.z, f.w));
+                  } else {
+                    uint8_t* dst = p.out + ((int64_t)rw.q_token * p.out_row_stride + (int64_t)rhead * D + c) * 4;
+                    *reinterpret_cast<float4*>(dst) = f;
+                  }
+                } else {
+                  *reinterpret_cast<float4*>(p.partial_o + ((int64_t)rslot * p.hq_count + rhead) * D + c) = f;
+                }
+              }
+            }
+            if (valid && X == 0 && wq == 0) {
+              if (slot < 0) {
+                if (p.lse) p.lse[(int64_t)head * p.total_q + row.q_token] = lse_v;
+              } else {
+                p.partial_lse[(int64_t)slot * p.hq_count + head] = lse_v;
+              }
             }
           }
           c4_end = 0;   // nothing left for the generic store path below
