@@ -28,13 +28,15 @@ for v in a.variants:
 b = bench.make_workload(a.cfg, 0)
 runners = {}
 for v in a.variants:
-    flags = v.split(":")[1] if ":" in v else "default"
+    flags = ":".join(v.split(":")[1:]) if ":" in v else "default"
     if flags not in runners:
+        if flags.count(":"):   # <lib>:<flags>:<PI_DPACK_ROWS> (planner A/B hook)
+            os.environ["PI_DPACK_ROWS"] = flags.split(":")[1]
         pk._lib = libs[v.split(":")[0]]
         if flags == "default":
             os.environ.pop("PI_BENCH_PLAN_FLAGS", None)
         else:
-            os.environ["PI_BENCH_PLAN_FLAGS"] = flags
+            os.environ["PI_BENCH_PLAN_FLAGS"] = flags.split(":")[0]
         rr = bench.Runner(b, "cuda", 0, b.hkv, seed=b.seed)
         rr.step(0)
         runners[flags] = rr
@@ -45,7 +47,7 @@ times = {v: [] for v in a.variants}
 for rep in range(a.reps + 3):
     for v in a.variants:
         pk._lib = libs[v.split(":")[0]]
-        r = runners[v.split(":")[1] if ":" in v else "default"]
+        r = runners[":".join(v.split(":")[1:]) if ":" in v else "default"]
         pb = r.pbs[0]
         flush.fill_(rep & 0xff)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
