@@ -458,25 +458,39 @@ def decode_loop(dev, h0, hc, seed_rank, args):
     kn = torch.randn((bd.n, bd.hkv, bd.d), device=dev).to(torch.bfloat16)
     vn = torch.randn_like(kn)
 
-    def loop_once():
-        pbl.replan()
-        pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0)   # consolidation
+    def loop_once(graph=False):
+        if graph:   # every step's device part as one CUDA graph replay (PackedBatch.graph_run)
+            pbl.replan(upload=False)
+            pbl.graph_run(ql, outl, None, tl["k_paged"], tl["v_paged"], tl["block_table"], hkv_begin=h0,
+                          relayout=True)
+        else:
+            pbl.replan()
+            pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0)   # consolidation
         for k in range(1, loop_steps):
             pbl.append(kn, vn, hkv_begin=h0)
-            pbl.replan(appended=np.full(bd.n, k, np.int32))
-            pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0, relayout=False)
-    loop_once()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    loop_once()
-    e1.record()
-    torch.cuda.synchronize()
-    lms = e0.elapsed_time(e1) / loop_steps
+            if graph:
+                pbl.replan(appended=np.full(bd.n, k, np.int32), upload=False)
+                pbl.graph_run(ql, outl, None, hkv_begin=h0)
+            else:
+                pbl.replan(appended=np.full(bd.n, k, np.int32))
+                pbl.run(ql, tl["k_paged"], tl["v_paged"], tl["block_table"], outl, hkv_begin=h0, relayout=False)
+
+    def timed_loop(graph):
+        loop_once(graph)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        loop_once(graph)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / loop_steps
+    lms = timed_loop(False)
+    lms_graph = timed_loop(True)
     kv_tokens = sum(int(bd.kv_len.sum()) + k * bd.n for k in range(loop_steps)) / loop_steps
     lbytes = 2 * kv_tokens * hc * bd.d * 2 + 2 * bd.n * hc * rr * bd.d * 2
     out = {"workload": bd.name + " (BASELINE.json configs[2])", "steps": loop_steps, "headroom": delta,
            "ms_per_step_amortized": lms, "step_gbs_amortized": lbytes / (lms * 1e-3) / 1e9,
+           "graph_ms_per_step_amortized": lms_graph,
            "note": "consolidation (relayout) once per 32 steps; per step: append + plan_step + upload + "
                    "decode attention + merge"}
     del tl, pbl
@@ -810,8 +824,9 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
     rd.relayout = False
     rms = timed_steps(rd, steps, args.warmup, dist_on) / steps
     rk = rd.kernel_ms()
+    gms = graph_resident(rd, steps, args.warmup)
     if dist_on:
-        rms, rk = max_over_ranks(dev, rms, rk)
+        rms, rk, gms = max_over_ranks(dev, rms, rk, gms)
     c = rd.pbs[0].plan.c
     paged = paged_decode(bd, rd, dev, h0, hc, steps, args.warmup, dist_on)
     out = {"ms_per_step": dms, "kernel_ms": dec_ms, "merge_ms": mrg_ms, "kv_bytes": kvb, "qo_bytes": qob,
@@ -822,6 +837,7 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
            "step_latency": rd.step_latency(), "gpu_launches": rd.launches_per_step * steps,
            "clocks": sampler.window(*win) if win else None,
            "resident": {"ms_per_step": rms, "kernel_ms": rk, "step_over_kernel": rms / rk,
+                        "graph_ms_per_step": gms,
                         "step_gbs": (kvb + qob) / (rms * 1e-3) / 1e9,
                         "gpu_launches_per_step": rd.launches_per_step - 1,
                         "note": "KV resident in the group-contiguous layout: plan + upload (+ row expansion) "
@@ -830,6 +846,27 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
            "paged": paged}
     del rd
     return out
+
+
+def graph_resident(rd, steps, warmup):
+    """The resident decode step with its device part as ONE CUDA graph launch
+    (PackedBatch.graph_run: plan upload + row expansion + attention + merge): per step the host
+    planner writes the tables, one graph replay runs them.  Device time per step (CUDA events)."""
+    import torch
+    pb = rd.pbs[0]
+    for _ in range(max(warmup, 2)):
+        pb.replan(upload=False)
+        pb.graph_run(rd.q, rd.out, rd.lse, hkv_begin=rd.hkv_begin)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        pb.replan(upload=False)
+        pb.graph_run(rd.q, rd.out, rd.lse, hkv_begin=rd.hkv_begin)
+    e1.record()
+    torch.cuda.synchronize()
+    pb.replan()                                    # back to eager uploads for later sections
+    return e0.elapsed_time(e1) / steps
 
 
 def paged_decode(bd, rd, dev, h0, hc, steps, warmup, dist_on):

@@ -439,9 +439,11 @@ class PackedBatch:
             # zero once; the in-kernel merge leaves them zero after every launch
             self.merge_counters = torch.zeros(nm, dtype=torch.int32, device=self.device)
 
-    def replan(self, stream=None, appended=None):
+    def replan(self, stream=None, appended=None, upload: bool = True):
         """Host planning + plan upload (the per-step host part of the hot path).  `appended`:
-        decode tokens appended per request since the last consolidation (packinfer_plan_step)."""
+        decode tokens appended per request since the last consolidation (packinfer_plan_step).
+        upload=False: host planning only - the upload is then part of the step's CUDA graph
+        (graph_run)."""
         import torch
         kv_len, q_len, prefix_id, prefix_len = self.args
         s = self._slot = 1 - self._slot
@@ -454,13 +456,74 @@ class PackedBatch:
         self._arenas[s] = self.plan.arena          # may have grown
         if int(self.plan.c.device_arena_bytes) > self.dev_arena.numel():
             self.dev_arena = torch.empty(int(self.plan.c.device_arena_bytes), dtype=torch.uint8, device=self.device)
-        self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
+        if upload:
+            self.dp = packinfer_plan_upload(self.plan, self.dev_arena, stream)
         # appended tokens can push a decode suffix across a decode_chunk boundary: more decode items,
         # more partial slots (the kernels index partial_o / partial_lse by the plan's slot ids)
         self._ensure_partials()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream() if stream is None else stream)
         self._events[s] = ev
+
+    # ------------------------------------------------------------------ CUDA graph of a step
+    def _graph_key(self, tensors, relayout):
+        """What a captured step depends on besides the plan tables' CONTENTS: the plan's shape
+        (table counts and arena offsets fix every kernel parameter and device pointer) and the
+        buffers the graph reads and writes."""
+        c = self.plan.c
+        shape = (int(c.arena_bytes), int(c.device_arena_bytes), int(c.n_segs), int(c.n_rows),
+                 int(c.n_prefill_work), int(c.n_decode_work), int(c.n_spans), int(c.n_merges),
+                 int(c.n_partial_slots), int(c.n_copies), int(c.buffer_tokens), int(c.rows_offset),
+                 int(c.sched_offset), int(c.total_q))
+        ptrs = tuple(0 if t is None else int(t.data_ptr()) for t in tensors)
+        return shape + ptrs + (bool(relayout), _arena_ptr(self._arenas[self._slot]), int(self.dev_arena.data_ptr()),
+                               int(self.partial_o.data_ptr()))
+
+    def graph_run(self, q, out, lse=None, k_paged=None, v_paged=None, block_table=None, hkv_begin: int = 0,
+                  relayout: bool = False):
+        """The device part of one step as ONE CUDA graph launch on the current stream: plan upload
+        (H2D of the host tables + row expansion) [+ KV relayout] + ONE attention launch + LSE merge.
+        Call after replan(upload=False).  A graph is captured per host-arena slot and replayed while
+        the plan's shape and the buffers stay the same (e.g. every decode step between regroups,
+        whose tables change only in content); a new shape captures another graph (up to 16 are kept,
+        so a loop that cycles through a few shapes replays all of them).  The memcpy node reads the
+        pinned host arena at replay time, so the tables of THIS step are what the kernels see."""
+        import torch
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}                     # (slot, key) -> graph, most recent last
+        tens = (q, out, lse, k_paged, v_paged, block_table, self.k_buf, self.v_buf)
+        gk = (self._slot,) + self._graph_key(tens, relayout)
+        g = self._graphs.pop(gk, None)
+        self.graph_captures = getattr(self, "graph_captures", 0)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            cur = torch.cuda.current_stream()
+            cs = torch.cuda.Stream(device=self.device)
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
+                g.capture_begin()
+                try:
+                    dp = packinfer_plan_upload(self.plan, self.dev_arena, cs)
+                    if relayout:
+                        packinfer_relayout_kv(dp, k_paged, v_paged, block_table, self.k_buf, self.v_buf, hkv_begin,
+                                              self.hkv, cs)
+                    packinfer_attention(dp, q, self.k_buf, self.v_buf, out, lse, self.partial_o, self.partial_lse,
+                                        self.r, 0.0, cs)
+                    packinfer_merge(dp, self.partial_o, self.partial_lse, out, lse, cs)
+                finally:
+                    g.capture_end()
+            cur.wait_stream(cs)
+            self.graph_captures += 1
+            self._dp_of = getattr(self, "_dp_of", {})
+            self._dp_of[gk] = dp
+            while len(self._graphs) >= 16:        # a decode loop cycles through a few plan shapes
+                self._graphs.pop(next(iter(self._graphs)))
+        self._graphs[gk] = g
+        self.dp = self._dp_of[gk]
+        g.replay()
+        ev = torch.cuda.Event()
+        ev.record()
+        self._events[self._slot] = ev            # the replay's memcpy reads this host arena
 
     def append(self, k_new, v_new, hkv_begin: int = 0, stream=None):
         """Write one new decode token per request into its headroom slot (current plan)."""

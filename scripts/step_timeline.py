@@ -7,6 +7,7 @@ import torch
 import bench
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4_decode"
 resident = "resident" in sys.argv
+graph = "graph" in sys.argv
 b = bench.make_workload(name, 0)
 r = bench.Runner(b, "cuda", 0, b.hkv, seed=b.seed)
 for i in range(5):
@@ -14,9 +15,19 @@ for i in range(5):
 torch.cuda.synchronize()
 r.relayout = not resident
 from torch.profiler import profile, ProfilerActivity
+pb = r.pbs[0]
+if graph:   # the resident step with its device part as one CUDA graph (PackedBatch.graph_run)
+    for _ in range(3):
+        pb.replan(upload=False)
+        pb.graph_run(r.q, r.out, r.lse)
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for i in range(5, 10):
-        r.step(i, time_kernel=True)
+        if graph:
+            pb.replan(upload=False)
+            pb.graph_run(r.q, r.out, r.lse)
+        else:
+            r.step(i, time_kernel=True)
     torch.cuda.synchronize()
     torch.cuda.synchronize()
 ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
@@ -28,4 +39,5 @@ for e in ev:
     gap = (e.time_range.start - prev) if prev is not None else 0
     print(f"{s:9.1f} us  +gap {gap:6.1f}  dur {d:8.1f}  {e.name[:70]}")
     prev = e.time_range.end
-print("event-timed: attention", r.kernel_ms(), "merge", r.merge_ms())
+if not graph:
+    print("event-timed: attention", r.kernel_ms(), "merge", r.merge_ms())

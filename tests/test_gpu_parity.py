@@ -373,6 +373,46 @@ def test_decode_loop_append():
     assert regroups >= 1                              # the headroom (4) ran out within 10 steps
 
 
+def test_graph_step_equals_eager():
+    """A decode loop whose device part runs as ONE CUDA graph per step (PackedBatch.graph_run: plan
+    upload + relayout + attention + merge captured, replayed with each step's new host tables) is
+    bitwise equal to the eager launches, including steps whose plan shape changes (appended tokens
+    cross a decode_chunk boundary -> re-capture)."""
+    from paper_2602_06072_b200 import packinfer as pk
+    b = W.random_batch(405, n=10, max_len=600, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=1.0)
+    steps, delta = 5, 6
+    t = W.make_tensors(b, device="cuda", extra_tokens=steps)
+    r = b.hq // b.hkv
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    mk = lambda: pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16,
+                                "cuda", capacity=700, headroom=delta, decode_chunk=128)
+    pe, pg = mk(), mk()
+    qb = torch.empty((b.n, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
+    oe = torch.empty((b.n, b.hq, b.d), dtype=torch.bfloat16, device="cuda")
+    og, le, lg = torch.empty_like(oe), torch.empty((b.hq, b.n), device="cuda"), torch.empty((b.hq, b.n), device="cuda")
+    captures = 0
+    for k in range(steps):
+        qb.copy_(torch.randn((b.n, b.hq, b.d), generator=g, device="cuda").to(torch.bfloat16))
+        if k > 0:
+            kn = torch.randn((b.n, b.hkv, b.d), generator=g, device="cuda").to(torch.bfloat16)
+            vn = torch.randn((b.n, b.hkv, b.d), generator=g, device="cuda").to(torch.bfloat16)
+            pe.append(kn, vn)
+            pg.append(kn, vn)
+            app = np.full(b.n, k, np.int32)
+            pe.replan(appended=app)
+            pg.replan(appended=app, upload=False)
+        else:
+            pg.replan(upload=False)
+        pe.run(qb, t["k_paged"], t["v_paged"], t["block_table"], oe, le, relayout=(k == 0))
+        pg.graph_run(qb, og, lg, t["k_paged"], t["v_paged"], t["block_table"], relayout=(k == 0))
+        captures = pg.graph_captures
+        torch.cuda.synchronize()
+        assert torch.equal(oe.view(torch.int16), og.view(torch.int16)), k
+        assert torch.equal(le, lg), k
+    assert captures < steps          # at least one step replayed an existing graph
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_decode_group_sharding_one_batch(world):
     """Group sharding of ONE decode batch (shard.RankPlan), the ranks simulated one after the other
