@@ -1224,6 +1224,7 @@ def main():
     if not args.no_prefix:
         sp = {"workload": "cfg4 shared prefix: 128 requests over 8 prompts x 2048 tokens (BASELINE.json configs[3])"}
         sp["decode"] = section_decode("cfg4_decode", dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_rank)
+        sp["decode"]["traffic"] = json.load(open(tf)).get("decode_cfg4_attention_dram_bytes") if os.path.exists(tf) else None
         sp["suffix_prefill"] = section_prefill("cfg4_prefill", dev, h0, hc, args, peaks, dist_on, sampler,
                                                seed_rank)
         result["shared_prefix"] = sp

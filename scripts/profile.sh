@@ -16,9 +16,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:pack
   -o $OUT/prefill $B --no-decode > $OUT/prefill.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 15 -c 1 \
   -o $OUT/decode $B > $OUT/decode.log 2>&1
+# configs[3] decode: the 4th attention launch of the in-process harness (current library as variants/libpi_cur.so)
+cp paper_2602_06072_b200/libpackinfer.so variants/libpi_cur.so
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:packed_attention -s 3 -c 1 \
+  -o $OUT/decode_cfg4 python scripts/ab_inproc.py cfg4_decode cur --reps 2 > $OUT/decode_cfg4.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:relayout -s 1 -c 1 \
   -o $OUT/relayout $B --no-decode > $OUT/relayout.log 2>&1
-for k in prefill decode relayout; do
+for k in prefill decode decode_cfg4 relayout; do
   ncu -i $OUT/$k.ncu-rep --page raw --csv > $OUT/${k}_raw.csv 2>/dev/null
 done
 ncu -i $OUT/prefill.ncu-rep --page source --csv --print-source sass > $OUT/prefill_sass.csv 2>/dev/null

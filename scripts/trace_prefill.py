@@ -76,3 +76,14 @@ if len(cta):
     print(f"CTAs {len(cta)}: entry us max {st.max():.2f}; exit us min {en.min():.2f} median {np.median(en):.2f} "
           f"p90 {np.percentile(en, 90):.2f} max {en.max():.2f}; units/CTA min {cta[:, 2].min()} max {cta[:, 2].max()}")
     print("  busy fraction (sum of CTA spans / (CTAs x launch span)):", round(float((en - st).sum() / (len(cta) * en.max())), 3))
+
+# per-unit timeline of CTA 0 (cycles relative to the first event): MMA issuer unit start, Q landed,
+# K landed, last MMA committed; Q gather waits QFREE / got it / issued; softmax warp 4 unit start,
+# first S landed, O landed (epilogue start), O read + stored, epilogue done
+print("unit  mma_start  mma_gotQ  mma_gotK  mma_done  ql_waitF  ql_gotF  ql_done  sm_start sm_gotS0  sm_epi  sm_Oread sm_epidone  | gotQ-prev_done  epi(cycles)")
+prev_done = None
+for i in range(min(nu, 40)):
+    r = U[i]
+    gap = (r[1] - prev_done) if prev_done else 0
+    print(f"{i:4d} " + " ".join(f"{(v - u0 if v else -1):9d}" for v in r[:12]) + f"  | {gap:8d} {r[11] - r[9]:8d}")
+    prev_done = r[3]
