@@ -154,6 +154,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #ifndef PI_SLICE_ROWS
 #define PI_SLICE_ROWS 32   // lane-sliced single-tile units: up to this many rows (one lane quarter)
 #endif
+#ifndef PI_Q_BOX
+#define PI_Q_BOX 1   // Q tiles of consecutive tokens as 3D TMA boxes (else every tile via gather4)
+#endif
 #ifndef PI_DEC_S_AFTER_EPI
 #define PI_DEC_S_AFTER_EPI 0
 #endif
@@ -322,7 +325,8 @@ __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
 template <int D, bool F32, int UK>
 __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
     packed_attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
-                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ) {
+                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ,
+                            const __grid_constant__ CUtensorMap tmQB) {
   using C = AttnCfg<D, F32, UK>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -367,6 +371,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
     prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmQB);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -678,17 +683,39 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       const bool sl = unit_sliced<UK, F32>(u);
       const int gpq = (rows + 3) >> 2;
       const int groups = sl ? 4 * gpq : gpq;
-      if (lane == 0) mbar_arrive_expect_tx(&bar[B_QFULL], (uint32_t)(nt * groups * C::ATOMS * 512));
-      __syncwarp();
-      if (lane < groups) {
-        const int gi = sl ? lane % gpq : lane;
-        const int dst_group = sl ? 8 * (lane / gpq) + gi : lane;
-        int32_t ri[4];
+      const int gi = sl ? lane % gpq : lane;
+      int32_t ri[4];
+      bool run = true;   // this lane's rows are tokens tok0 + row index (one contiguous run of Q)
+      int tok0 = 0;
+      {
+        const int32_t t0 = p.rows[u.wk.row_begin].q_token;
+        tok0 = t0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const pi_row row = p.rows[u.wk.row_begin + min(4 * gi + e, rows - 1)];
           ri[e] = row.q_token * p.q_heads_stride + u.head0 + (row.out & 15);
+          if (lane < groups && 4 * gi + e < rows) run = run && row.q_token == t0 + 4 * gi + e && (row.out & 15) == 0;
         }
+      }
+      // A tile whose rows are consecutive tokens of Q (a long request's 128 query positions, or
+      // adjacent short ones) is ONE 3D box per 128-byte atom column (tmQB: d x head x token, 128
+      // tokens; rows past the tile's row_count are computed and discarded, past the end of Q
+      // zero-filled); other tiles gather 4 rows per TMA op.  A gather4 op takes ~120 issue cycles,
+      // so a 2-tile gather (128 ops) kept the next unit's S waiting ~8k cycles at every unit start.
+      const bool box = PI_Q_BOX && !sl && __all_sync(0xffffffffu, run);
+      if (lane == 0)
+        mbar_arrive_expect_tx(&bar[B_QFULL], box ? (uint32_t)(nt * C::TILE_BYTES) : (uint32_t)(nt * groups * C::ATOMS * 512));
+      __syncwarp();
+      if (box) {
+        if (lane == 0) {
+          for (int X = 0; X < nt; ++X)
+#pragma unroll
+            for (int a = 0; a < C::ATOMS; ++a)
+              tma_load_3d(smem + C::OFF_Q + X * C::TILE_BYTES + a * C::ATOM_BYTES, &tmQB, &bar[B_QFULL],
+                          a * C::ATOM_ELEMS, u.head0 + X, tok0);
+        }
+      } else if (lane < groups) {
+        const int dst_group = sl ? 8 * (lane / gpq) + gi : lane;
         for (int X = 0; X < nt; ++X) {
           uint8_t* dst = smem + C::OFF_Q + X * C::TILE_BYTES + dst_group * 512;
 #pragma unroll
@@ -1582,7 +1609,7 @@ unsigned long long* g_debug_trace = nullptr;
 
 template <int D, bool F32, int UK>
 static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                               const CUtensorMap& tmQ, int grid, cudaStream_t stream) {
+                               const CUtensorMap& tmQ, const CUtensorMap& tmQB, int grid, cudaStream_t stream) {
   using C = AttnCfg<D, F32, UK>;
   if constexpr (F32 && UK != 2) {
     return fail(PI_EUNSUP, "fp32 operands run single-tile units only");
@@ -1591,7 +1618,7 @@ static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, cons
     pi_status s = set_max_dynamic_smem(reinterpret_cast<const void*>(packed_attention_kernel<D, F32, UK>),
                                        smem_opt_in, C::SMEM);
     if (s != PI_OK) return s;
-    packed_attention_kernel<D, F32, UK><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ);
+    packed_attention_kernel<D, F32, UK><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ, tmQB);
     return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
   }
 }
@@ -1676,6 +1703,13 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   const uint32_t qbox[3] = {(uint32_t)C::ATOM_ELEMS, 1u, 1u};
   s = encode_tmap_2d(&tmQ, dt, q, qdims, qstrides, qbox, CU_TENSOR_MAP_SWIZZLE_128B);
   if (s != PI_OK) return s;
+  // the same Q as (d, head, token) boxes of 128 tokens for tiles whose rows are consecutive tokens
+  CUtensorMap tmQB;
+  const uint64_t bdims[3] = {(uint64_t)D, (uint64_t)p.q_heads_stride, (uint64_t)dp->total_q};
+  const uint64_t bstrides[2] = {(uint64_t)C::ROW_BYTES, (uint64_t)q_row_stride * C::ES};
+  const uint32_t bbox[3] = {(uint32_t)C::ATOM_ELEMS, 1u, 128u};
+  s = encode_tmap_3d(&tmQB, dt, q, bdims, bstrides, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (s != PI_OK) return s;
 
   const int64_t total = (int64_t)p.total_p + (int64_t)p.n_work_d * p.units_d;
   const int grid = (int)std::min<int64_t>(total, num_sms());
@@ -1686,9 +1720,9 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   // has pair units only, a decode-only launch (or fp32 operands) single-tile units only
   const bool pairs_only = !F32 && p.n_work_d == 0 && (r % 2) == 0;
   const bool singles_only = F32 || p.n_work_p == 0 || r == 1;
-  if (pairs_only) return launch_kernel<D, F32, 1>(p, tmK, tmV, tmQ, grid, stream);
-  if (singles_only) return launch_kernel<D, F32, 2>(p, tmK, tmV, tmQ, grid, stream);
-  return launch_kernel<D, F32, 3>(p, tmK, tmV, tmQ, grid, stream);
+  if (pairs_only) return launch_kernel<D, F32, 1>(p, tmK, tmV, tmQ, tmQB, grid, stream);
+  if (singles_only) return launch_kernel<D, F32, 2>(p, tmK, tmV, tmQ, tmQB, grid, stream);
+  return launch_kernel<D, F32, 3>(p, tmK, tmV, tmQ, tmQB, grid, stream);
 }
 
 static pi_status attention_entry(int mode, const pi_device_plan* dp, const void* q, int64_t q_row_stride,
