@@ -157,9 +157,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #ifndef PI_Q_BOX
 #define PI_Q_BOX 1   // Q tiles of consecutive tokens as 3D TMA boxes (else every tile via gather4)
 #endif
-#ifndef PI_DEC_S_AFTER_EPI
-#define PI_DEC_S_AFTER_EPI 0
-#endif
 #ifndef PI_DEC_NSV
 #define PI_DEC_NSV 3   // V stages of decode-only (single-tile) launches: V is held until P.V
 #endif
@@ -603,12 +600,6 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           // ---- single-tile unit: S/P regions alternate per tile so S(j+1) overlaps softmax(j)
           const bool s128_pro = PI_SINGLE_S128 == 1 || PI_SINGLE_S128 == 2 || (PI_SINGLE_S128 == 3 && n <= 4);
           const bool s128_body = PI_SINGLE_S128 == 1 || (PI_SINGLE_S128 == 3 && n <= 4);
-          if (PI_DEC_S_AFTER_EPI) {
-            // A/B: S(0) of this unit only after the previous unit's epilogue released O (keeps the
-            // SS MMA's shared-memory operand stream off the epilogue's exchange)
-            mbar_wait(&bar[B_OFREE0], (ix & 1) ^ 1);
-            mbar_wait(&bar[B_OFREE1], (ix & 1) ^ 1);
-          }
           issue_s(0, 0, t, s128_pro);
           trace_ev(p, t, 27);
           commit(B_KFREE0 + (t % C::NSK));
