@@ -240,6 +240,33 @@ def test_plan_options_keep_layout_and_coverage(seed, flags):
     check_merge_map(hp, q, r)
 
 
+@pytest.mark.parametrize("name", ["cfg3", "cfg4_decode"])
+def test_default_config_packs_decode_items_within_slice_rows(name):
+    """packinfer_default_config packs short decode suffixes (PI_PLAN_DPACK): a packed item - rows of
+    several requests with different key intervals - never exceeds 32 rows (the kernel lane-slices
+    decode units of <= 32 rows) nor a decode_chunk-long hull, and the layout (Parts 1-2) is the
+    same as without the option."""
+    b = W.make_batch(name)
+    r = b.hq // b.hkv
+    cfg = pk.default_config(gqa_ratio=r)
+    assert cfg.flags == pk.PI_PLAN_DPACK
+    hp = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, cfg)
+    h0 = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, pk.default_config(gqa_ratio=r, flags=0))
+    for f in ("pieces", "offsets", "groups", "copies"):
+        assert np.array_equal(getattr(hp, f), getattr(h0, f)), f
+    segs = hp.segs
+    packed = 0
+    for w in hp.decode_work:
+        mine = [sg for sg in segs if w["row_begin"] <= sg["row_begin"] < w["row_begin"] + w["row_count"]]
+        intervals = {(int(sg["lo"]), int(sg["hi"])) for sg in mine}
+        if len({int(sg["q_token"]) for sg in mine}) > 1 and len(intervals) > 1:   # a packed suffix item
+            packed += 1
+            assert int(w["row_count"]) <= 32
+            assert int(w["span_count"]) == 1 and int(hp.spans[w["span_begin"]]["len"]) <= cfg.decode_chunk
+    assert packed > 0
+    assert int(hp.c.n_decode_work) < int(h0.c.n_decode_work)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_paged_plan_covers_logical_tokens(seed):
     """PI_PLAN_PAGED (NEXT-4 ablation): decode items over each request's logical tokens; every
