@@ -41,9 +41,6 @@
 #include "packinfer.h"
 #include "sm100.cuh"
 
-#ifndef PI_P_F16
-#define PI_P_F16 0   // experiment: P packed as fp16 against bf16 V (idesc a_fmt = f16, b_fmt = bf16)
-#endif
 #ifndef PI_P_ROUNDED_SUM
 #define PI_P_ROUNDED_SUM 2   // O normalised by the row sum of the bf16-rounded P: 1 = FHADD.BF16, 2 = PRMT + FADD2; 0 = exact sum
 #endif
@@ -203,7 +200,9 @@ struct AttnCfg {
   // the 32B-atom swizzle, so warp 3 stages V^T (K-major, SWIZZLE_128B) instead.
   // P is rounded to bf16 (P <= 2^8 by the lazy rescale) and V is the bitwise bf16 copy in the group
   // buffers: P.V is kind::f16 with bf16 x bf16, V the MN-major B operand (reading R13).
-  static constexpr uint32_t IDESC_PV = F32 ? idesc_make(FMT, 128, D, 0, 0) : idesc_make2(PI_P_F16 ? 0 : 1, 1, 128, D, 0, 1);
+  static constexpr uint32_t IDESC_PV = F32 ? idesc_make(FMT, 128, D, 0, 0) : idesc_make2(1, 1, 128, D, 0, 1);
+  // (a_fmt = f16 against b_fmt = bf16 - fp16 P with the bf16 V - is an illegal instruction on
+  // sm_100a: kind::f16 needs both operands of one type, profiles/r03a)
   static constexpr int VT_ATOM_BYTES = D * 128;       // fp32 V^T: D rows x 32 keys
   static constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
   // warps 0..ROLE-1: TMA producer, MMA issuer, Q gather (+ V^T staging for fp32); then two softmax
