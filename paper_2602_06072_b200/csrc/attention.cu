@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <type_traits>
 
@@ -65,6 +66,22 @@
 #ifndef PI_POLY_PAIRS
 #define PI_POLY_PAIRS 2   // of every 8 score pairs, this many take exp2 on the FMA pipe (A/B: scripts/ab_poly.sh)
 #endif
+
+// Debug build (-DPI_CHECKS=1, tests/test_gpu_checks.py): device-side bounds checks on every plan
+// table entry the kernel dereferences (work items, spans, rows, partial slots, heads); a failed
+// check prints its id and traps.  compute-sanitizer is not available on every GPU pool; these
+// checks cover the indices it would.
+#ifndef PI_CHECKS
+#define PI_CHECKS 0
+#endif
+#define PI_CHECK(cond, id)                                                                             \
+  do {                                                                                                 \
+    if (PI_CHECKS && !(cond)) {                                                                        \
+      printf("packinfer device check %d failed: block %d thread %d\n", (int)(id), (int)blockIdx.x,       \
+             (int)threadIdx.x);                                                                        \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
 
 namespace pi {
 
@@ -106,6 +123,7 @@ struct AttnParams {
   const int32_t* block_table;   // NULL = group-contiguous buffers
   int32_t max_blocks, page, kv_head0;
   uint32_t* sched;              // [0] dynamic unit counter, [1] CTAs exited; zero on entry and on exit
+  int32_t n_partial_slots;      // (PI_CHECKS bounds)
 };
 
 // One paged-mode tile: logical keys [k0, k0 + 128) of block-table row `row` = 128 consecutive slots
@@ -315,6 +333,8 @@ __device__ __forceinline__ Unit get_unit(const AttnParams& p, int w) {
   }
   if (UK == 1) u.has_b = true;
   if (UK == 2) u.has_b = false;
+  PI_CHECK(u.wk.row_count >= 1 && u.wk.row_count <= 128 && u.wk.span_count >= 1 && u.wk.n_ktiles >= 1, 1);
+  PI_CHECK(u.head0 >= 0 && u.head0 + (u.has_b ? 1 : 0) < p.hq_count, 2);
   return u;
 }
 
@@ -416,6 +436,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       }
       for (int s = 0; s < u.wk.span_count; ++s) {
         const pi_span sp = s == 0 ? span0 : p.spans[u.wk.span_begin + s];
+        PI_CHECK(sp.begin >= 0 && sp.len >= 0 && (p.block_table != nullptr || sp.begin + sp.len <= p.buffer_tokens), 3);
         for (int k0 = sp.begin; k0 < sp.begin + sp.len; k0 += 128, ++t) {
           const int st = t % C::NSK, sv = t % C::NSV;
           const uint32_t ph = (t / C::NSK) & 1, phv = (t / C::NSV) & 1;
@@ -685,6 +706,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
           const pi_row row = p.rows[u.wk.row_begin + min(4 * gi + e, rows - 1)];
           ri[e] = row.q_token * p.q_heads_stride + u.head0 + (row.out & 15);
           if (lane < groups && 4 * gi + e < rows) run = run && row.q_token == t0 + 4 * gi + e && (row.out & 15) == 0;
+          PI_CHECK(row.q_token >= 0 && row.q_token < p.total_q && u.head0 + (row.out & 15) + (nt - 1) < p.hq_count, 5);
         }
       }
       // A tile whose rows are consecutive tokens of Q (a long request's 128 query positions, or
@@ -902,6 +924,9 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       nu = get_unit<UK>(p, wn);
       const int ri = unit_sliced<UK, F32>(nu) ? lane : row_id;   // sliced: row `lane` in every quarter
       nrow = ri < nu.wk.row_count ? p.rows[nu.wk.row_begin + ri] : pi_row{0, 0, 0, 0};
+      PI_CHECK(ri >= nu.wk.row_count || (nrow.q_token >= 0 && nrow.q_token < p.total_q && nrow.lo <= nrow.hi &&
+                                         (nrow.out >> 4) - 1 < p.n_partial_slots && (nrow.out >> 4) >= 0),
+               4);
       nsp = p.spans[nu.wk.span_begin];
     };
     int w = ring_get(uring, bar, 0);
@@ -1248,6 +1273,7 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
       if (warp == C::ROLE && lane == 0) trace_unit(p, ix, 9);
       const int slot = (row.out >> 4) - 1;
       const int head = u.head0 + (u.has_b ? X : 0) + (row.out & 15);
+      PI_CHECK(!valid || (slot < p.n_partial_slots && head < p.hq_count), 6);
       // pair units: out = O_X / l.  Single units: the two warpgroups hold (m, l) of key halves
       // 0..63 / 64..127 of every tile with partial accumulators O_0 / O_1; merge them (reading
       // R10: M = max, w = 2^(m - M), L = sum w l) and let warpgroup X write output columns
@@ -1654,6 +1680,7 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   p.buffer_tokens = dp->buffer_tokens;
   p.trace = g_debug_trace;
   p.sched = dp->sched;
+  p.n_partial_slots = dp->n_partial_slots;
   p.merges = dp->merges;
   p.slot_merge = dp->slot_merge;
   // fp32 operands: warp 3 stages V^T, so the entry point merges with a separate launch instead

@@ -7,9 +7,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "device_common.h"
 #include "packinfer.h"
+
+#ifndef PI_CHECKS
+#define PI_CHECKS 0   // debug build: bounds checks on the merge table (see attention.cu)
+#endif
 
 namespace pi {
 
@@ -17,12 +22,19 @@ template <int D, bool F32>
 __global__ void __launch_bounds__(256) merge_kernel(const pi_merge* __restrict__ merges, int32_t n_merges,
                                                     const float* __restrict__ po, const float* __restrict__ pl,
                                                     int32_t hq, uint8_t* out, int64_t out_row_stride, float* lse,
-                                                    int32_t total_q) {
+                                                    int32_t total_q, int32_t n_slots) {
   const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (gw >= (int64_t)n_merges * hq) return;
   const int m = (int)(gw / hq), h = (int)(gw % hq);
   const pi_merge mg = merges[m];
+#if PI_CHECKS
+  if (!(mg.slot_begin >= 0 && mg.slot_count >= 1 && mg.slot_begin + mg.slot_count <= n_slots && mg.q_token >= 0 &&
+        mg.q_token < total_q)) {
+    printf("packinfer device check 7 failed: merge %d\n", m);
+    __trap();
+  }
+#endif
   float M = -INFINITY;
   for (int b = lane; b < mg.slot_count; b += 32) M = fmaxf(M, __ldcg(&pl[(int64_t)(mg.slot_begin + b) * hq + h]));
 #pragma unroll
@@ -91,16 +103,16 @@ extern "C" pi_status packinfer_merge(const pi_device_plan* dp, const float* part
   uint8_t* o = static_cast<uint8_t*>(out);
   if (dt == PI_BF16 && head_dim == 128)
     merge_kernel<128, false><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,
-                                                     out_row_stride, lse, dp->total_q);
+                                                     out_row_stride, lse, dp->total_q, dp->n_partial_slots);
   else if (dt == PI_BF16 && head_dim == 64)
     merge_kernel<64, false><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,
-                                                    out_row_stride, lse, dp->total_q);
+                                                    out_row_stride, lse, dp->total_q, dp->n_partial_slots);
   else if (dt == PI_FP32 && head_dim == 64)
     merge_kernel<64, true><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,
-                                                   out_row_stride, lse, dp->total_q);
+                                                   out_row_stride, lse, dp->total_q, dp->n_partial_slots);
   else if (dt == PI_FP32 && head_dim == 128)
     merge_kernel<128, true><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,
-                                                    out_row_stride, lse, dp->total_q);
+                                                    out_row_stride, lse, dp->total_q, dp->n_partial_slots);
   else
     return fail(PI_EUNSUP, "head_dim must be 64 or 128; dtype PI_BF16 or PI_FP32");
   pi_status s = cuda_check(cudaGetLastError(), "merge_kernel launch");
