@@ -36,10 +36,14 @@ struct RelayoutParams {
   int64_t buf_head_bytes;     // buffer_tokens * d * es
   uint8_t* kb;
   uint8_t* vb;
+  int32_t tpw;                // buffer tokens per warp: 1, or 128 / chunks when a token is < 128 chunks
 };
 
 #ifndef PI_RL_TPW
 #define PI_RL_TPW 1
+#endif
+#ifndef PI_RL_MULTI
+#define PI_RL_MULTI 1   // several tokens per warp when a token has < 128 chunks of 16 B (few local KV heads)
 #endif
 constexpr int RL_TPW = PI_RL_TPW;   // consecutive buffer tokens per warp (one copy-entry search)
 constexpr int RL_U = 4;             // 16-byte chunks per lane in flight per tensor
@@ -63,9 +67,60 @@ __device__ __forceinline__ int find_copy(const int64_t* __restrict__ ext_prefix,
   return lo;
 }
 
+// Few local KV heads (KV-head sharding: 1-4 heads per rank) make a token only 16-64 chunks of
+// 16 B, so one token per warp leaves most lanes idle behind a chain of dependent loads (copy-entry
+// search, copy entry, block table, data).  Then a warp takes p.tpw = 128 / chunks consecutive
+// tokens and each lane 4 (token, chunk) pairs of them: every warp moves 2 x 2 KB per chain.
+__device__ __forceinline__ void relayout_multi(const RelayoutParams& p, int64_t g0, int lane) {
+  const int64_t total = __ldg(&p.ext_prefix[p.n_copies]);
+  const int c0 = find_copy(p.ext_prefix, p.n_copies, g0, lane);
+  const int64_t row_bytes = (int64_t)p.head_chunks * 16;
+  uint4 kv[RL_U], vv[RL_U];
+  int64_t dsts[RL_U];
+  bool live[RL_U];
+#pragma unroll
+  for (int u = 0; u < RL_U; ++u) {
+    const int f = u * 32 + lane;
+    const int64_t g = g0 + f / p.chunks;
+    const int i = f % p.chunks;
+    live[u] = f < p.tpw * p.chunks && g < total;
+    kv[u] = vv[u] = make_uint4(0, 0, 0, 0);
+    dsts[u] = 0;
+    if (live[u]) {
+      int c = c0;
+      while (c + 1 < p.n_copies && g >= __ldg(&p.ext_prefix[c + 1])) ++c;   // a copy ends inside the warp
+      const pi_copy cp = p.copies[c];
+      const int64_t off = g - __ldg(&p.ext_prefix[c]);
+      const int h = i / p.head_chunks, cc = i % p.head_chunks;
+      dsts[u] = h * p.buf_head_bytes + (cp.dst + off) * row_bytes + (int64_t)cc * 16;
+      if (off < cp.len) {   // else headroom: zeros
+        const int row = cp.src_kind == 0 ? cp.src_id : p.n_requests + cp.src_id;
+        const int64_t j = cp.src_begin + off;
+        const int blk = __ldg(&p.bt[(int64_t)row * p.max_blocks + j / p.page]);
+        const int64_t src = ((int64_t)blk * p.page + j % p.page) * p.token_bytes + p.head_off_bytes;
+        kv[u] = __ldg(reinterpret_cast<const uint4*>(p.kp + src) + i);
+        vv[u] = __ldg(reinterpret_cast<const uint4*>(p.vp + src) + i);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < RL_U; ++u) {
+    if (live[u]) {
+      *reinterpret_cast<uint4*>(p.kb + dsts[u]) = kv[u];
+      *reinterpret_cast<uint4*>(p.vb + dsts[u]) = vv[u];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) relayout_kernel(const RelayoutParams p) {
-  const int64_t g0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RL_TPW;
   const int lane = threadIdx.x & 31;
+  if (p.tpw > 1) {
+    const int64_t g0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * p.tpw;
+    if (g0 >= __ldg(&p.ext_prefix[p.n_copies])) return;
+    relayout_multi(p, g0, lane);
+    return;
+  }
+  const int64_t g0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RL_TPW;
   // cells to write = the copy list's own cell count (== buffer_tokens for a batch plan; a rank's
   // share under group sharding, shard.RankPlan, is smaller: the grid covers buffer_tokens)
   const int64_t total = __ldg(&p.ext_prefix[p.n_copies]);
@@ -209,7 +264,9 @@ extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void*
   p.buf_head_bytes = dp->buffer_tokens * head_dim * es;
   p.kb = static_cast<uint8_t*>(k_buf);
   p.vb = static_cast<uint8_t*>(v_buf);
-  const int64_t blocks = (p.total + 8 * RL_TPW - 1) / (8 * RL_TPW);
+  p.tpw = (PI_RL_MULTI && p.chunks < 32 * RL_U) ? (32 * RL_U) / p.chunks : 1;
+  const int64_t per_warp = p.tpw > 1 ? p.tpw : RL_TPW;
+  const int64_t blocks = (p.total + 8 * per_warp - 1) / (8 * per_warp);
   if (blocks > 0x7fffffff) return fail(PI_EINVAL, "buffer too large");
   relayout_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   pi_status s = cuda_check(cudaGetLastError(), "relayout_kernel launch");

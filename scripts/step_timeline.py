@@ -9,7 +9,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg4_decode"
 resident = "resident" in sys.argv
 graph = "graph" in sys.argv
 b = bench.make_workload(name, 0)
-r = bench.Runner(b, "cuda", 0, b.hkv, seed=b.seed)
+heads1 = "h1" in sys.argv   # one KV head (the per-rank share of KV-head sharding at N = 8), pipelined steps
+r = bench.Runner(b, "cuda", 0, 1 if heads1 else b.hkv, seed=b.seed, pipeline=heads1)
 for i in range(5):
     r.step(i)
 torch.cuda.synchronize()
