@@ -47,6 +47,10 @@ struct RelayoutParams {
 #endif
 constexpr int RL_TPW = PI_RL_TPW;   // consecutive buffer tokens per warp (one copy-entry search)
 constexpr int RL_U = 4;             // 16-byte chunks per lane in flight per tensor
+#ifndef PI_RLM_U
+#define PI_RLM_U 4
+#endif
+constexpr int RLM_U = PI_RLM_U;     // the same for the several-tokens-per-warp path
 
 // Largest c with ext_prefix[c] <= g (ext_prefix strictly increasing, ext_prefix[0] = 0 <= g):
 // 32-ary warp search, each round narrows [lo, hi] ~32x with one coalesced probe per lane, so the
@@ -75,11 +79,11 @@ __device__ __forceinline__ void relayout_multi(const RelayoutParams& p, int64_t 
   const int64_t total = __ldg(&p.ext_prefix[p.n_copies]);
   const int c0 = find_copy(p.ext_prefix, p.n_copies, g0, lane);
   const int64_t row_bytes = (int64_t)p.head_chunks * 16;
-  uint4 kv[RL_U], vv[RL_U];
-  int64_t dsts[RL_U];
-  bool live[RL_U];
+  uint4 kv[RLM_U], vv[RLM_U];
+  int64_t dsts[RLM_U];
+  bool live[RLM_U];
 #pragma unroll
-  for (int u = 0; u < RL_U; ++u) {
+  for (int u = 0; u < RLM_U; ++u) {
     const int f = u * 32 + lane;
     const int64_t g = g0 + f / p.chunks;
     const int i = f % p.chunks;
@@ -104,7 +108,7 @@ __device__ __forceinline__ void relayout_multi(const RelayoutParams& p, int64_t 
     }
   }
 #pragma unroll
-  for (int u = 0; u < RL_U; ++u) {
+  for (int u = 0; u < RLM_U; ++u) {
     if (live[u]) {
       *reinterpret_cast<uint4*>(p.kb + dsts[u]) = kv[u];
       *reinterpret_cast<uint4*>(p.vb + dsts[u]) = vv[u];
@@ -264,7 +268,7 @@ extern "C" pi_status packinfer_relayout_kv(const pi_device_plan* dp, const void*
   p.buf_head_bytes = dp->buffer_tokens * head_dim * es;
   p.kb = static_cast<uint8_t*>(k_buf);
   p.vb = static_cast<uint8_t*>(v_buf);
-  p.tpw = (PI_RL_MULTI && p.chunks < 32 * RL_U) ? (32 * RL_U) / p.chunks : 1;
+  p.tpw = (PI_RL_MULTI && p.chunks < 32 * RLM_U) ? (32 * RLM_U) / p.chunks : 1;
   const int64_t per_warp = p.tpw > 1 ? p.tpw : RL_TPW;
   const int64_t blocks = (p.total + 8 * per_warp - 1) / (8 * per_warp);
   if (blocks > 0x7fffffff) return fail(PI_EINVAL, "buffer too large");
