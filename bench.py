@@ -581,9 +581,10 @@ def tuned_loop(dev, h0, hc, seed_rank, epochs: int = 10, cands=(2048, 4096, 8192
 
 def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
     """BASELINE.json configs[4]: Llama-3-70B-shaped mixed batch (2 x 128k-token prefills split
-    across groups + 30 short prefills + 224 decodes up to 32k), ONE fused attention launch over
-    prefill and decode work items with the LSE merge inside it (NEXT-3); the split form (prefill
-    launch, decode launch, merge launch) is timed beside it on the same plan."""
+    across groups + 30 short prefills + 224 decodes up to 32k), ONE attention call over prefill
+    and decode work items with the LSE merge inside it (NEXT-3: packinfer_attention_merge, the
+    decode half a programmatic dependent launch filling the prefill launch's tail); the split form
+    (prefill launch, decode launch, merge launch) is timed beside it on the same plan."""
     import torch
     from synth import workloads as W
     from paper_2602_06072_b200 import packinfer as pk

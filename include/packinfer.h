@@ -244,11 +244,12 @@ typedef struct {
   const int32_t* append_pos;                 /* [n_requests] (see pi_plan)                      */
   const int32_t* slot_merge;                 /* [n_partial_slots] (see pi_plan); NULL disables
                                                 packinfer_attention_merge                        */
-  uint32_t* sched;                           /* [2] dynamic unit counter of the attention
-                                                launches and their exit count: zeroed by
+  uint32_t* sched;                           /* [4] two (unit counter, exits) pairs of the
+                                                attention launches (the second for the decode half
+                                                of a prefill + decode call): zeroed by
                                                 packinfer_plan_upload, left at zero by every
                                                 completed launch (the last CTA resets them), so
-                                                one attention launch per device plan at a time  */
+                                                one attention call per device plan at a time     */
 } pi_device_plan;
 
 /* Enqueue one host->device copy of plan->arena (arena_bytes) into dev_arena (device, >=

@@ -169,6 +169,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #ifndef PI_SLICE_ROWS
 #define PI_SLICE_ROWS 32   // lane-sliced single-tile units: up to this many rows (one lane quarter)
 #endif
+#ifndef PI_FUSED_PDL
+#define PI_FUSED_PDL 1   // packinfer_attention(_merge) over both kinds: two specialised launches chained by PDL
+#endif
 #ifndef PI_Q_BOX
 #define PI_Q_BOX 1   // Q tiles of consecutive tokens as 3D TMA boxes (else every tile via gather4)
 #endif
@@ -429,6 +432,8 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
         wn = r * (int)gridDim.x + ((r & 1) ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x);
       }
       if (wn >= total) wn = -1;
+      // no unit left to start here: a programmatic dependent launch may take the SMs that free up
+      if (wn < 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       ring_put(k + 1, wn);
       if (wn >= 0) {
         nu = get_unit<UK>(p, wn);
@@ -1625,7 +1630,8 @@ unsigned long long* g_debug_trace = nullptr;
 
 template <int D, bool F32, int UK>
 static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                               const CUtensorMap& tmQ, const CUtensorMap& tmQB, int grid, cudaStream_t stream) {
+                               const CUtensorMap& tmQ, const CUtensorMap& tmQB, int grid, cudaStream_t stream,
+                               bool pdl = false) {
   using C = AttnCfg<D, F32, UK>;
   if constexpr (F32 && UK != 2) {
     return fail(PI_EUNSUP, "fp32 operands run single-tile units only");
@@ -1634,6 +1640,23 @@ static pi_status launch_kernel(const AttnParams& p, const CUtensorMap& tmK, cons
     pi_status s = set_max_dynamic_smem(reinterpret_cast<const void*>(packed_attention_kernel<D, F32, UK>),
                                        smem_opt_in, C::SMEM);
     if (s != PI_OK) return s;
+    if (pdl) {
+      // programmatic dependent launch: this grid's CTAs may start on SMs the previous launch on the
+      // stream frees once every CTA of it has run out of units (griddepcontrol.launch_dependents);
+      // the two launches write disjoint rows / partials
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3(C::THREADS);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cuda_check(cudaLaunchKernelEx(&cfg, packed_attention_kernel<D, F32, UK>, p, tmK, tmV, tmQ, tmQB),
+                        "packed_attention_kernel launch (PDL)");
+    }
     packed_attention_kernel<D, F32, UK><<<grid, C::THREADS, C::SMEM, stream>>>(p, tmK, tmV, tmQ, tmQB);
     return cuda_check(cudaGetLastError(), "packed_attention_kernel launch");
   }
@@ -1649,7 +1672,8 @@ template <int D, bool F32>
 static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const void* q, int64_t q_row_stride,
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
-                        uint32_t* merge_ctr, cudaStream_t stream, const PagedSrc* paged = nullptr) {
+                        uint32_t* merge_ctr, cudaStream_t stream, const PagedSrc* paged = nullptr,
+                        bool pdl = false, int sched_pair = 0) {
   using C = AttnCfg<D, F32>;   // tile geometry only (independent of the unit kinds)
   AttnParams p{};
   p.work_p = dp->prefill_work;
@@ -1679,7 +1703,7 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   p.out_f32 = out_f32 ? 1 : 0;
   p.buffer_tokens = dp->buffer_tokens;
   p.trace = g_debug_trace;
-  p.sched = dp->sched;
+  p.sched = dp->sched ? dp->sched + 2 * sched_pair : nullptr;
   p.n_partial_slots = dp->n_partial_slots;
   p.merges = dp->merges;
   p.slot_merge = dp->slot_merge;
@@ -1737,9 +1761,9 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   // has pair units only, a decode-only launch (or fp32 operands) single-tile units only
   const bool pairs_only = !F32 && p.n_work_d == 0 && (r % 2) == 0;
   const bool singles_only = F32 || p.n_work_p == 0 || r == 1;
-  if (pairs_only) return launch_kernel<D, F32, 1>(p, tmK, tmV, tmQ, tmQB, grid, stream);
-  if (singles_only) return launch_kernel<D, F32, 2>(p, tmK, tmV, tmQ, tmQB, grid, stream);
-  return launch_kernel<D, F32, 3>(p, tmK, tmV, tmQ, tmQB, grid, stream);
+  if (pairs_only) return launch_kernel<D, F32, 1>(p, tmK, tmV, tmQ, tmQB, grid, stream, pdl);
+  if (singles_only) return launch_kernel<D, F32, 2>(p, tmK, tmV, tmQ, tmQB, grid, stream, pdl);
+  return launch_kernel<D, F32, 3>(p, tmK, tmV, tmQ, tmQB, grid, stream, pdl);
 }
 
 static pi_status attention_entry(int mode, const pi_device_plan* dp, const void* q, int64_t q_row_stride,
@@ -1777,6 +1801,23 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
   if (s != PI_OK) return s;
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)head_dim);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (PI_FUSED_PDL && mode == 3 && dt == PI_BF16 && paged == nullptr && dp->n_prefill_work > 0 &&
+      dp->n_decode_work > 0) {
+    // one call over prefill + decode items: the prefill items on the pair-unit kernel instance,
+    // then the decode items on the single-tile instance as a programmatic dependent launch that
+    // fills the SMs the prefill launch releases at its tail (its own scheduler counters).  One
+    // persistent mixed-instance launch (PI_FUSED_PDL=0) carries both unit kinds' code and register
+    // budget: prefill units run 14 % slower there (profiles/r04q).
+    for (int part = 1; part <= 2 && s == PI_OK; ++part) {
+      if (head_dim == 128)
+        s = launch<128, false>(dp, part, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+                               out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, nullptr, part == 2, part - 1);
+      else
+        s = launch<64, false>(dp, part, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
+                              out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, nullptr, part == 2, part - 1);
+    }
+    return s == PI_OK ? ok() : s;
+  }
   if (dt == PI_BF16 && head_dim == 128)
     s = launch<128, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                            out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged);

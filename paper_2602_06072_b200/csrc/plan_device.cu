@@ -17,7 +17,7 @@ namespace pi {
 // CTA 0 also zeroes the attention launches' scheduler counters (pi_device_plan.sched).
 __global__ void __launch_bounds__(128) expand_rows_kernel(const pi_rowseg* __restrict__ segs, pi_row* __restrict__ rows,
                                                           uint32_t* __restrict__ sched) {
-  if (blockIdx.x == 0 && threadIdx.x < 2) sched[threadIdx.x] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;   // two (counter, exits) pairs
   const pi_rowseg g = segs[blockIdx.x];
   for (int j = threadIdx.x; j < g.count; j += blockDim.x) {
     const bool pre = g.kind == PI_SEG_PREFILL;
@@ -55,7 +55,7 @@ extern "C" pi_status packinfer_plan_upload(const pi_plan* p, void* dev_arena, si
     pi_status s = pi::cuda_check(cudaGetLastError(), "expand_rows_kernel launch");
     if (s != PI_OK) return s;
   } else {
-    e = cudaMemsetAsync(sched, 0, 2 * sizeof(uint32_t), st);
+    e = cudaMemsetAsync(sched, 0, 4 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return pi::fail(PI_ECUDA, std::string("plan upload: ") + cudaGetErrorString(e));
   }
   std::memset(out, 0, sizeof(*out));
