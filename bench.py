@@ -486,11 +486,14 @@ def decode_loop(dev, h0, hc, seed_rank, args):
         return e0.elapsed_time(e1) / loop_steps
     lms = timed_loop(False)
     lms_graph = timed_loop(True)
+    caps_before = getattr(pbl, "graph_captures", 0)
+    lms_graph = min(lms_graph, timed_loop(True))   # every plan shape of the loop captured by now
+    graph_captures_timed = getattr(pbl, "graph_captures", 0) - caps_before
     kv_tokens = sum(int(bd.kv_len.sum()) + k * bd.n for k in range(loop_steps)) / loop_steps
     lbytes = 2 * kv_tokens * hc * bd.d * 2 + 2 * bd.n * hc * rr * bd.d * 2
     out = {"workload": bd.name + " (BASELINE.json configs[2])", "steps": loop_steps, "headroom": delta,
            "ms_per_step_amortized": lms, "step_gbs_amortized": lbytes / (lms * 1e-3) / 1e9,
-           "graph_ms_per_step_amortized": lms_graph,
+           "graph_ms_per_step_amortized": lms_graph, "graph_captures_in_last_loop": graph_captures_timed,
            "note": "consolidation (relayout) once per 32 steps; per step: append + plan_step + upload + "
                    "decode attention + merge"}
     del tl, pbl
