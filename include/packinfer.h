@@ -308,11 +308,15 @@ PI_API pi_status packinfer_attention_decode(const pi_device_plan* dp, const void
                                      float* partial_o, float* partial_lse, pi_stream_t stream);
 
 /* Fused form (NEXT-3; BASELINE.json north star "one packed attention kernel launch
- * per layer ... covering both prefill and decode"): ONE persistent launch over the prefill AND
- * the decode work items of the plan (prefill units first, the cheaper decode units fill the
- * tail).  Arguments, layouts and errors as above; q/out hold every request's rows (q_len = 1
- * for decode requests) in the caller's varlen order.  Equivalent to
- * packinfer_attention_prefill followed by packinfer_attention_decode.                         */
+ * per layer ... covering both prefill and decode"): ONE call over the prefill AND the decode
+ * work items of the plan.  For bf16 operands with both kinds present it is two persistent
+ * launches of the kernel's specialised instances - prefill units, then decode units as a
+ * programmatic dependent launch whose CTAs fill the SMs the prefill launch frees at its tail;
+ * otherwise (and when built with -DPI_FUSED_PDL=0) one persistent launch of the mixed instance
+ * (prefill units first, the cheaper decode units fill the tail).  Arguments, layouts and errors
+ * as above; q/out hold every request's rows (q_len = 1 for decode requests) in the caller's
+ * varlen order.  Results are bitwise those of packinfer_attention_prefill followed by
+ * packinfer_attention_decode.                                                                   */
 PI_API pi_status packinfer_attention(const pi_device_plan* dp, const void* q, int64_t q_row_stride,
                                      const void* k_buf, const void* v_buf, int32_t hkv_count,
                                      int32_t gqa_ratio, int32_t head_dim, float softmax_scale,
