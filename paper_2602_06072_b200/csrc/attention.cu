@@ -124,6 +124,7 @@ struct AttnParams {
   int32_t max_blocks, page, kv_head0;
   uint32_t* sched;              // [0] dynamic unit counter, [1] CTAs exited; zero on entry and on exit
   int32_t n_partial_slots;      // (PI_CHECKS bounds)
+  int32_t pdl_wait;             // launched as a programmatic dependent: griddepcontrol.wait after set-up
 };
 
 // One paged-mode tile: logical keys [k0, k0 + 128) of block-table row `row` = 128 consecutive slots
@@ -171,6 +172,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #endif
 #ifndef PI_FUSED_PDL
 #define PI_FUSED_PDL 1   // packinfer_attention(_merge) over both kinds: two specialised launches chained by PDL
+#endif
+#ifndef PI_STEP_PDL
+#define PI_STEP_PDL 1   // attention / merge launches as programmatic dependents (set-up overlaps the previous kernel)
 #endif
 #ifndef PI_Q_BOX
 #define PI_Q_BOX 1   // Q tiles of consecutive tokens as 3D TMA boxes (else every tile via gather4)
@@ -396,6 +400,10 @@ __global__ void __launch_bounds__(AttnCfg<D, F32, UK>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // launched as a programmatic dependent of the previous kernel on the stream (relayout, or the
+  // previous step's merge): the set-up above overlapped its tail; nothing it writes is read or
+  // written before this point
+  if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const int total = p.total_p + p.n_work_d * p.units_d;
   // Register budget per warpgroup (setmaxnreg, at the top of each role's branch): the role warps
@@ -1673,7 +1681,7 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
                         const void* k_buf, const void* v_buf, int32_t hkv_count, int32_t r, float scale,
                         void* out, int64_t out_row_stride, float* lse, float* partial_o, float* partial_lse,
                         uint32_t* merge_ctr, cudaStream_t stream, const PagedSrc* paged = nullptr,
-                        bool pdl = false, int sched_pair = 0) {
+                        bool pdl = false, int sched_pair = 0, bool pdl_wait = false) {
   using C = AttnCfg<D, F32>;   // tile geometry only (independent of the unit kinds)
   AttnParams p{};
   p.work_p = dp->prefill_work;
@@ -1704,6 +1712,8 @@ static pi_status launch(const pi_device_plan* dp, int mode, bool out_f32, const 
   p.buffer_tokens = dp->buffer_tokens;
   p.trace = g_debug_trace;
   p.sched = dp->sched ? dp->sched + 2 * sched_pair : nullptr;
+  p.pdl_wait = pdl_wait ? 1 : 0;
+  pdl = pdl || pdl_wait;
   p.n_partial_slots = dp->n_partial_slots;
   p.merges = dp->merges;
   p.slot_merge = dp->slot_merge;
@@ -1811,16 +1821,18 @@ static pi_status attention_entry(int mode, const pi_device_plan* dp, const void*
     for (int part = 1; part <= 2 && s == PI_OK; ++part) {
       if (head_dim == 128)
         s = launch<128, false>(dp, part, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                               out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, nullptr, part == 2, part - 1);
+                               out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, nullptr, part == 2, part - 1,
+                               PI_STEP_PDL && part == 1);
       else
         s = launch<64, false>(dp, part, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                              out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, nullptr, part == 2, part - 1);
+                              out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, nullptr, part == 2, part - 1,
+                              PI_STEP_PDL && part == 1);
     }
     return s == PI_OK ? ok() : s;
   }
   if (dt == PI_BF16 && head_dim == 128)
     s = launch<128, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
-                           out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged);
+                           out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged, false, 0, PI_STEP_PDL);
   else if (dt == PI_BF16 && head_dim == 64)
     s = launch<64, false>(dp, mode, out_f32, q, q_row_stride, k_buf, v_buf, hkv_count, gqa_ratio, scale, out,
                           out_row_stride, lse, partial_o, partial_lse, merge_ctr, st, paged);

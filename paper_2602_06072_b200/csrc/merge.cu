@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const pi_merge* __restrict__
                                                     const float* __restrict__ po, const float* __restrict__ pl,
                                                     int32_t hq, uint8_t* out, int64_t out_row_stride, float* lse,
                                                     int32_t total_q, int32_t n_slots) {
+  // launched as a programmatic dependent of the attention launch that wrote the partials
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (gw >= (int64_t)n_merges * hq) return;
@@ -101,9 +103,23 @@ extern "C" pi_status packinfer_merge(const pi_device_plan* dp, const float* part
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dt == PI_BF16_OUT_F32) dt = PI_FP32;  // output element type is what the merge writes
   uint8_t* o = static_cast<uint8_t*>(out);
-  if (dt == PI_BF16 && head_dim == 128)
-    merge_kernel<128, false><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,
-                                                     out_row_stride, lse, dp->total_q, dp->n_partial_slots);
+  if (dt == PI_BF16 && head_dim == 128) {
+    // programmatic dependent launch: the merge's launch and CTA start overlap the attention
+    // launch's tail; griddepcontrol.wait in the kernel orders its reads after it
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, merge_kernel<128, false>, dp->merges, dp->n_merges, partial_o,
+                                       partial_lse, hq_count, o, out_row_stride, lse, dp->total_q,
+                                       dp->n_partial_slots);
+    if (e != cudaSuccess) return cuda_check(e, "merge_kernel launch (PDL)");
+  }
   else if (dt == PI_BF16 && head_dim == 64)
     merge_kernel<64, false><<<blocks, 256, 0, st>>>(dp->merges, dp->n_merges, partial_o, partial_lse, hq_count, o,
                                                     out_row_stride, lse, dp->total_q, dp->n_partial_slots);
