@@ -613,3 +613,37 @@ def test_paged_decode_ablation(name):
         packed = pk.packinfer_plan(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, pk.default_config(gqa_ratio=r))
         paged_keys = int(sum(s["len"] for s in pb.plan.spans))
         assert int(packed.c.copy_tokens) < paged_keys == int(b.kv_len.sum())
+
+
+def test_repeated_launches_bitwise_stable():
+    """The dynamic scheduler's counters are zeroed at plan upload and reset by the last CTA of every
+    launch, and attention / merge launches are programmatic dependents of the kernel before them:
+    many back-to-back launches of different kinds and grid sizes on one device plan (fused with its
+    PDL-chained decode half, split prefill / decode, KV-head slices, in-kernel merge) must each
+    reproduce their first result bit for bit."""
+    from paper_2602_06072_b200 import packinfer as pk
+    b = W.random_batch(406, n=16, max_len=900, hq=8, hkv=2, d=128, n_prefix=2, decode_frac=0.5)
+    t = W.make_tensors(b, device="cuda")
+    r = b.hq // b.hkv
+    pb = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, b.hkv, r, b.d, torch.bfloat16, "cuda",
+                        capacity=600, headroom=2, decode_chunk=256)
+    pb1 = pk.PackedBatch(b.kv_len, b.q_len, b.prefix_id, b.prefix_len, 1, r, b.d, torch.bfloat16, "cuda",
+                         capacity=600, headroom=2, decode_chunk=256)
+    variants = [("fused", pb, 0, dict(fused=True)), ("split", pb, 0, dict(fused=False)),
+                ("merge_in_kernel", pb, 0, dict(fused=True, kernel_merge=True)), ("head1", pb1, 1, dict(fused=True))]
+    ref = {}
+    for rep in range(6):
+        for name, p_, h0, kw in variants:
+            hc = p_.hkv
+            out = torch.full((b.total_q, hc * r, b.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+            lse = torch.full((hc * r, b.total_q), float("nan"), dtype=torch.float32, device="cuda")
+            p_.run(t["q"][:, h0 * r:(h0 + hc) * r], t["k_paged"], t["v_paged"], t["block_table"], out, lse,
+                   hkv_begin=h0, relayout=(rep == 0), **kw)
+            got = (out.view(torch.int16).clone(), lse.view(torch.int32).clone())
+            if name not in ref:
+                ref[name] = got
+            else:
+                assert torch.equal(got[0], ref[name][0]) and torch.equal(got[1], ref[name][1]), (rep, name)
+    # the three full-head variants agree with each other too
+    assert torch.equal(ref["fused"][0], ref["split"][0]) and torch.equal(ref["fused"][0], ref["merge_in_kernel"][0])
+    assert torch.equal(ref["head1"][0], ref["fused"][0][:, r:2 * r])
