@@ -215,6 +215,7 @@ class Runner:
         # relayout + row expansion (inside the plan upload) + one attention launch + merge
         self.launches_per_step = 1 + (c.n_segs > 0) + 1 + (SEPARATE_MERGE and c.n_merges > 0)
         self.kernel_events = []
+        self.relayout_events = []
         self.step_events = []
 
     def begin(self, ev):
@@ -243,8 +244,14 @@ class Runner:
             es.record(aux)
         pb.replan(aux)                               # host planner + async upload + row expansion
         if self.relayout:
+            if time_kernel:
+                r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                r0.record(aux)
             pk.packinfer_relayout_kv(pb.dp, t["k_paged"], t["v_paged"], t["block_table"], pb.k_buf,
                                      pb.v_buf, self.hkv_begin, self.hkv_count, aux)
+            if time_kernel:
+                r1.record(aux)
+                self.relayout_events.append((r0, r1))
         self.ready[k].record(aux)
         self.stream.wait_event(self.ready[k])
         if time_kernel:
@@ -281,6 +288,11 @@ class Runner:
         v = [a.elapsed_time(b) for a, b, _ in self.kernel_events]
         return sum(v) / len(v) if v else 0.0
 
+    def relayout_ms(self):
+        """Average time of the step's relayout launch (consolidation, paged -> group layout)."""
+        v = [a.elapsed_time(b) for a, b in self.relayout_events]
+        return sum(v) / len(v) if v else 0.0
+
     def merge_ms(self):
         """Average time of the separate LSE-merge launch after it (0 with the in-kernel merge)."""
         v = [b.elapsed_time(c) for _, b, c in self.kernel_events]
@@ -300,6 +312,7 @@ def timed_steps(runner, steps, warmup, dist_on, window=None):
         dist.barrier()
     torch.cuda.synchronize()
     runner.kernel_events.clear()
+    runner.relayout_events.clear()
     runner.step_events.clear()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
@@ -819,9 +832,9 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
     steps = max(10, args.steps)
     win = []
     dms = timed_steps(rd, steps, args.warmup, dist_on, win) / steps
-    dec_ms, mrg_ms = rd.kernel_ms(), rd.merge_ms()
+    dec_ms, mrg_ms, rl_ms = rd.kernel_ms(), rd.merge_ms(), rd.relayout_ms()
     if dist_on:
-        dms, dec_ms, mrg_ms = max_over_ranks(dev, dms, dec_ms, mrg_ms)
+        dms, dec_ms, mrg_ms, rl_ms = max_over_ranks(dev, dms, dec_ms, mrg_ms, rl_ms)
     ach = (kvb + qob) / (dec_ms * 1e-3) / 1e9
     # KV resident in the group layout (the producer writes new tokens there, packinfer_append_kv):
     # the step is host plan + upload + ONE attention launch with the merge inside - no relayout
@@ -833,7 +846,16 @@ def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_
         rms, rk, gms = max_over_ranks(dev, rms, rk, gms)
     c = rd.pbs[0].plan.c
     paged = paged_decode(bd, rd, dev, h0, hc, steps, args.warmup, dist_on)
+    c0 = rd.pbs[0].plan.c
+    # relayout bytes = 2 (K, V) x copied tokens x Hkv d 2 B x 2 (read + write); merge
+    # bytes = partials (o and lse, fp32) + the merged rows' bf16 outputs
+    rl_bytes = 2 * int(c0.copy_tokens) * hc * bd.d * 2 * 2
+    mg_bytes = int(c0.n_partial_slots) * hc * (bd.hq // bd.hkv) * (bd.d + 1) * 4 + \
+        int(c0.n_merges) * hc * (bd.hq // bd.hkv) * bd.d * 2
     out = {"ms_per_step": dms, "kernel_ms": dec_ms, "merge_ms": mrg_ms, "kv_bytes": kvb, "qo_bytes": qob,
+           "relayout": {"ms": rl_ms, "bytes": rl_bytes, "gbs": rl_bytes / (rl_ms * 1e-3) / 1e9 if rl_ms else None},
+           "merge": {"ms": mrg_ms, "bytes": mg_bytes, "gbs": mg_bytes / (mrg_ms * 1e-3) / 1e9 if mrg_ms else None,
+                     "note": "event-timed launch incl. its launch gap; partials are mostly evicted from L2 by the KV stream"},
            "achieved_gbs": ach,
            "peak_gbs": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"], "bound": "hbm",
            "step_gbs": (kvb + qob) / (dms * 1e-3) / 1e9, "work_items": int(c.n_decode_work),
