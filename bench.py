@@ -1235,7 +1235,7 @@ def main():
         gbytes = full.numel() * full.element_size()
         result["gather"] = {"ms": gms, "bytes_out": gbytes, "step_ms_with_gather": ms_step + gms,
                             "efficiency_with_gather": t1 / (world * (ms_step + gms)),
-                            "note": "NCCL all_gather_into_tensor of head-major O slabs + layout copy"}
+                            "note": f"{dist.get_backend()} all-gather of head-major O slabs (NCCL: all_gather_into_tensor) + layout copy"}
         del full, rg
 
     if not args.no_decode:
