@@ -457,6 +457,7 @@ def decode_loop(dev, h0, hc, seed_rank, args):
     delta = 32 (= max new tokens), then each step appends one token per request into its
     headroom, re-plans the execution domain on the host (packinfer_plan_step) and runs decode +
     merge.  Plus the online capacity tuner (NEXT-2) driving C on configs[3]."""
+    fresh_memory()
     import torch
     from synth import workloads as W
     from paper_2602_06072_b200 import packinfer as pk
@@ -601,6 +602,7 @@ def mixed_section(dev, h0, hc, rank, args, peaks, dist_on):
     and decode work items with the LSE merge inside it (NEXT-3: packinfer_attention_merge, the
     decode half a programmatic dependent launch filling the prefill launch's tail); the split form
     (prefill launch, decode launch, merge launch) is timed beside it on the same plan."""
+    fresh_memory()
     import torch
     from synth import workloads as W
     from paper_2602_06072_b200 import packinfer as pk
@@ -823,9 +825,21 @@ def max_over_ranks(dev, *vals):
     return [float(x) for x in t.tolist()]
 
 
+def fresh_memory():
+    """Between sections: release the previous sections' cached blocks so every section's buffers
+    are allocated the same way however much ran before it (the short configs[3] decode launch
+    otherwise varied with what earlier sections left in the caching allocator)."""
+    import gc
+    import torch
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
 def section_decode(name, dev, h0, hc, rank, args, peaks, dist_on, sampler, seed_rank):
     """A decode step (plan + upload + relayout + decode attention + merge) of one BASELINE batch on
     this rank's KV heads; GB/s = Eq. 5 KV bytes + Q/O bytes over the decode kernel time."""
+    fresh_memory()
     bd = make_workload(name, seed_rank)
     rd = Runner(bd, dev, h0, hc, seed=bd.seed)
     _, kvb, qob = algorithmic(bd, rd.pbs[0].plan.c, hc)
@@ -1057,6 +1071,7 @@ def library_decode(dev, name, ours_ms, timeit):
 def section_prefill(name, dev, h0, hc, args, peaks, dist_on, sampler, seed_rank):
     """A prefill step of one BASELINE batch on this rank's KV heads (TFLOP/s over the prefill
     kernel time and over the step)."""
+    fresh_memory()
     bp = make_workload(name, seed_rank)
     rp = Runner(bp, dev, h0, hc, seed=bp.seed)
     flops, _, _ = algorithmic(bp, rp.pbs[0].plan.c, hc)
